@@ -1,0 +1,231 @@
+"""Pin the CPU oracle (oracle/) to the reference before trusting it.
+
+Three layers of evidence, all CPU-only:
+  1. golden vectors produced by the reference itself (tests/golden/golden.npz,
+     written by tests/golden/make_golden.py from mossq 0.1.0);
+  2. the reference's own known-answer tests, restated (test_fp8.py,
+     test_quantize.py, test_gemm.py, test_optim.py, test_autoscale.py);
+  3. when /root/reference is mounted (this container), direct randomized
+     comparison against ``mossq``.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import numpy_ref as R
+
+
+# ---------------------------------------------------------------- codec
+def test_decode_tables_match_reference(golden):
+    for fmt, key in [(R.E4M3, "codec_decode_e4m3"), (R.E5M2, "codec_decode_e5m2")]:
+        got = R.decode_table(fmt)
+        want = golden[key]
+        assert np.array_equal(np.isnan(got), np.isnan(want))
+        ok = ~np.isnan(want)
+        assert np.array_equal(got[ok], want[ok])
+
+
+def test_encode_matches_reference_golden(golden, c_oracle):
+    x = golden["codec_encode_in"]
+    assert np.array_equal(R.fp8_encode(x, R.E4M3), golden["codec_encode_e4m3"])
+    assert np.array_equal(R.fp8_encode(x, R.E5M2), golden["codec_encode_e5m2"])
+    assert np.array_equal(c_oracle.e4m3(x), golden["codec_encode_e4m3"])
+
+
+def test_encode_anchors_ties_saturation():
+    # test_fp8.py:59-68, 84-87, 90-101, 124-127
+    tab = R.decode_table(R.E4M3)
+    for code, val in [(0x38, 1.0), (0x01, 2.0 ** -9), (0x08, 2.0 ** -6), (0x7E, 448.0),
+                      (0xB8, -1.0), (0x30, 0.5), (0x40, 2.0)]:
+        assert tab[code] == val
+    assert int(R.fp8_encode(np.float32(0.0))) == 0x00
+    assert int(R.fp8_encode(np.float32(-0.0))) == 0x80
+    for v in (449.0, 500.0, 8 * 448.0, 3e38):
+        assert tab[int(R.fp8_encode(np.float32(v)))] == 448.0
+        assert tab[int(R.fp8_encode(np.float32(-v)))] == -448.0
+    assert tab[int(R.fp8_encode(np.float32(25.0)))] == 24.0
+    assert tab[int(R.fp8_encode(np.float32(27.0)))] == 28.0
+
+
+def test_all_codes_roundtrip(c_oracle):
+    # test_fp8.py:35-45
+    tab = R.decode_table(R.E4M3)
+    codes = np.arange(256, dtype=np.uint8)
+    fin = np.isfinite(tab)
+    again = R.fp8_encode(tab[fin])
+    assert np.array_equal(again, codes[fin])
+    assert np.array_equal(c_oracle.e4m3(tab[fin]), codes[fin])
+
+
+def test_c_and_numpy_encoders_agree_on_random_bits(c_oracle):
+    rng = np.random.default_rng(0)
+    bits = rng.integers(0, 1 << 32, 2_000_000, dtype=np.uint64).astype(np.uint32)
+    x = bits.view(np.float32)
+    x = x[np.isfinite(x)]
+    assert np.array_equal(c_oracle.e4m3(x), R.fp8_encode(x))
+
+
+def test_e8m0_ceil_matches_golden(golden):
+    r = golden["codec_e8m0_in"]
+    assert np.array_equal(R.e8m0_encode_ceil(r), golden["codec_e8m0_ceil"])
+    # test_fp8.py:160-192 known answers
+    assert int(R.e8m0_encode_ceil(1.0)) == 127
+    assert float(R.e8m0_decode(R.e8m0_encode_ceil(0.75))) == 1.0
+    assert float(R.e8m0_decode(R.e8m0_encode_ceil(0.5))) == 0.5
+    assert int(R.e8m0_encode_ceil(2.0 ** -127)) == 0
+    assert int(R.e8m0_encode_ceil(2.0 ** 127)) == 254
+    with pytest.raises(OverflowError):
+        R.e8m0_encode_ceil(2.0 ** -130)
+
+
+# ---------------------------------------------------------------- quantizers
+def test_two_level_matches_golden(golden, c_oracle):
+    for name in list(golden["q2l_cases"]) + ["midrows"]:
+        x = golden[f"q2l_{name}_x"]
+        if name == "midrows":
+            rows = [R.quant_two_level(x[i:i + 1]) for i in range(x.shape[0])]
+            codes = np.concatenate([q.codes for q in rows])
+            micro = np.concatenate([q.micro_codes for q in rows])
+            g = np.array([q.global_scale for q in rows], np.float32)
+            cc = [c_oracle.quant_two_level(x[i:i + 1]) for i in range(x.shape[0])]
+            assert np.array_equal(np.concatenate([c[0] for c in cc]), golden["q2l_midrows_codes"])
+            assert np.array_equal(np.concatenate([c[1] for c in cc]), golden["q2l_midrows_micro"])
+        else:
+            q = R.quant_two_level(x)
+            codes, micro, g = q.codes, q.micro_codes, np.float32(q.global_scale)
+            c_codes, c_micro, c_g, st = c_oracle.quant_two_level(x)
+            assert st == 0, name
+            assert np.array_equal(c_codes, golden[f"q2l_{name}_codes"]), name
+            assert np.array_equal(c_micro, golden[f"q2l_{name}_micro"]), name
+            assert np.float32(c_g) == golden[f"q2l_{name}_g"], name
+        assert np.array_equal(codes, golden[f"q2l_{name}_codes"]), name
+        assert np.array_equal(micro, golden[f"q2l_{name}_micro"]), name
+        assert np.array_equal(g, golden[f"q2l_{name}_g"]), name
+
+
+def test_two_level_range_error(golden, c_oracle):
+    assert bool(golden["q2l_rangeerr_raises"])
+    x = golden["q2l_rangeerr_x"]
+    assert R.quant_two_level(x).e8m0_range_error
+    assert c_oracle.quant_two_level(x)[3] == 2
+
+
+def test_two_level_handworked():
+    # test_quantize.py:105-113
+    x = np.zeros(64, np.float32)
+    x[0], x[32] = 448.0, 0.875
+    q = R.quant_two_level(x)
+    assert q.global_scale == 1.0
+    assert q.micro_codes.tolist() == [127, 118]
+    assert np.array_equal(R.dequantize_two_level(q), x.astype(np.float64))
+
+
+def test_per_tensor_and_weight_encode(golden, c_oracle):
+    for name in ("exact", "two", "gauss", "w"):
+        codes, scale = R.quant_per_tensor(golden[f"qpt_{name}_x"])
+        assert np.array_equal(codes, golden[f"qpt_{name}_codes"])
+        assert scale == float(golden[f"qpt_{name}_scale"])
+    for i in range(3):
+        w, s = golden[f"wenc_{i}_w"], float(golden[f"wenc_{i}_s"])
+        codes, sat = R.encode_weight(w, s)
+        deq = R.fp8_decode(codes).astype(np.float64) * np.float64(np.float32(s))
+        deq = (R.fp8_decode(codes) * np.float32(s)).astype(np.float64)
+        assert np.array_equal(deq, golden[f"wenc_{i}_deq"])
+        assert sat == int(golden[f"wenc_{i}_sat"])
+        c_codes, c_sat = c_oracle.encode_scaled(w, s)
+        assert np.array_equal(c_codes, codes)
+
+
+# ---------------------------------------------------------------- GEMM
+@pytest.mark.parametrize("shape", ["64x64x64", "16x48x96", "128x128x256", "256x128x512"])
+def test_gemm_oracle_matches_reference(golden, shape):
+    t = f"gemm_{shape}"
+    q = R.TwoLevel(golden[t + "_xcodes"], float(golden[t + "_xg"]), golden[t + "_xmicro"])
+    out = R.gemm_mx_epilogue(golden[t + "_wcodes"], float(golden[t + "_wscale"]), q)
+    want = golden[t + "_out"]
+    assert np.linalg.norm(out - want) / np.linalg.norm(want) <= 1e-12
+    fast = R.gemm_f64(R.dequantize_per_tensor(golden[t + "_wcodes"], golden[t + "_wscale"]),
+                      R.dequantize_two_level(q))
+    assert np.linalg.norm(fast - want) / np.linalg.norm(want) <= 1e-10
+    # the oracle re-quantizes to the same operands
+    codes, scale = R.quant_per_tensor(golden[t + "_w"])
+    assert np.array_equal(codes, golden[t + "_wcodes"])
+    qx = R.quant_two_level(golden[t + "_x"])
+    assert np.array_equal(qx.codes, golden[t + "_xcodes"])
+
+
+# ---------------------------------------------------------------- AdamW + autoscale
+@pytest.mark.parametrize("tag", ["dec", "cpl", "nowd"])
+def test_adamw_matches_reference(golden, tag):
+    eta, wd, dec = golden[f"adam_{tag}_hp"]
+    st = R.adam_init(golden[f"adam_{tag}_w0"].shape, eta=float(eta), weight_decay=float(wd),
+                     decoupled_decay=bool(dec))
+    w = golden[f"adam_{tag}_w0"]
+    for i, g in enumerate(golden[f"adam_{tag}_g"]):
+        w, d = R.adamw_step(w, g, st)
+        assert np.allclose(w, golden[f"adam_{tag}_w"][i], rtol=0, atol=1e-15)
+        assert np.allclose(st.m, golden[f"adam_{tag}_m"][i], rtol=1e-14, atol=0)
+        assert np.allclose(st.v, golden[f"adam_{tag}_v"][i], rtol=1e-14, atol=0)
+
+
+def test_adamw_closed_forms():
+    # test_optim.py:34-46
+    st = R.adam_init((3,), eta=0.01, weight_decay=0.1)
+    w0 = np.array([1.0, -2.0, 0.5])
+    w = w0
+    for _ in range(25):
+        w, d = R.adamw_step(w, np.zeros(3), st)
+        assert np.all(d == 0)
+    assert np.allclose(w, w0 * (1 - 0.01 * 0.1) ** 25, rtol=1e-12)
+    st = R.adam_init((4,), eta=0.01, weight_decay=0.0, eps=1e-30)
+    w = np.zeros(4)
+    for _ in range(50):
+        w, d = R.adamw_step(w, np.full(4, 3.7), st)
+        assert np.allclose(np.abs(d), 0.01, rtol=1e-12)
+
+
+def test_autoscale_matches_reference(golden):
+    s = R.Schedule(s_t=0.01)
+    for _ in range(1000):
+        R.advance(s, 3e-4)
+    assert s.s_t == float(golden["sched_eq10_s"])
+    assert s.s_t == pytest.approx(0.01 + 0.3 / 448.0, abs=1e-12)      # test_autoscale.py:21-26
+    w = golden["sched_cos_w"]
+    s = R.Schedule(s_t=0.05, interval=120)
+    traj = []
+    for t, e in enumerate(golden["sched_cos_eta"]):
+        R.advance(s, float(e))
+        if R.rescale_due(s):
+            R.rescale(w * (1 + t / 1000.0), s)
+        traj.append(s.s_t)
+    assert np.array_equal(np.array(traj), golden["sched_cos_traj"])
+    assert R.jit_scale(w) == float(golden["sched_s0_jit"])
+
+
+# ---------------------------------------------------------------- direct vs mossq
+def test_randomized_against_live_reference(mossq):
+    from mossq.fp8 import E4M3, fp8_encode
+    from mossq.quantize import quant_two_level
+    from mossq.tensor import tensor_randn
+    rng = np.random.default_rng(123)
+    bits = rng.integers(0, 1 << 32, 400_000, dtype=np.uint64).astype(np.uint32).view(np.float32)
+    bits = bits[np.isfinite(bits)]
+    assert np.array_equal(R.fp8_encode(bits), fp8_encode(bits, E4M3))
+    for seed in range(6):
+        dist = ["gaussian", "outlier_injected", "laplace"][seed % 3]
+        x = tensor_randn([32, 256], seed=seed, dist=dist) * np.float32(10.0 ** (seed - 3))
+        a = R.quant_two_level(x)
+        b = quant_two_level(x, E4M3)
+        assert np.array_equal(a.codes, b.codes)
+        assert np.array_equal(a.micro_codes, b.micro_codes)
+        assert a.global_scale == b.global_scale
+
+
+def test_lr_schedule_matches_reference(mossq):
+    from mossq.train import TrainConfig, lr_at
+    cfg = TrainConfig(steps=1000, warmup_steps=100, lr_peak=0.01, quantize=False)
+    for step in (0, 5, 99, 100, 500, 999):
+        assert R.lr_at(step, lr_peak=0.01, warmup=100, steps=1000) == lr_at(cfg, step)
+    assert math.isclose(R.lr_at(999, lr_peak=0.01, warmup=100, steps=1000), 0.001, rel_tol=0.01)
