@@ -1,0 +1,130 @@
+/* moss_b200.h — C ABI of the B200-native MOSS FP8 training hot path.
+ *
+ * Plain pointers and sizes only: every pointer is a DEVICE pointer unless
+ * stated otherwise, every call is stream-ordered on the given cudaStream_t
+ * (passed as void*), nothing allocates, frees or synchronises.  The library
+ * is loaded with ctypes by paper_2511_05811_b200/_lib.py; INTEGRATION.md shows
+ * the binding a maintainer would add to the reference.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths under /root/reference/pkg/src/mossq/).
+ *
+ * Status codes mirror the reference's exception classes (errors.py:4-45):
+ * host-checkable problems are returned before launch; data-dependent ones
+ * (non-finite input, E8M0 exponent < -127) are OR-ed into *flags on the
+ * device and raised by the host at the next check.
+ */
+#ifndef MOSS_B200_H
+#define MOSS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum moss_status {
+    MOSS_OK = 0,
+    MOSS_ERR_SHAPE = 1,     /* InvalidShapeError   */
+    MOSS_ERR_VALUE = 2,     /* InvalidValueError   */
+    MOSS_ERR_ARGUMENT = 3,  /* InvalidArgumentError */
+    MOSS_ERR_E8M0 = 4,      /* E8m0RangeError      */
+    MOSS_ERR_CUDA = 5,      /* CUDA runtime failure */
+    MOSS_ERR_ALIGN = 6      /* pointer / stride alignment (InvalidArgumentError) */
+};
+
+enum moss_dtype { MOSS_F32 = 0, MOSS_BF16 = 1 };
+
+/* device flag bits */
+#define MOSS_FLAG_NONFINITE 1u      /* NaN/Inf input: quantize.py:88, fp8.py:139 */
+#define MOSS_FLAG_E8M0_RANGE 2u     /* e8m0 exponent < -127: fp8.py:219-222 */
+#define MOSS_FLAG_GRAD_NONFINITE 4u /* optim.py:89-90 */
+
+/* Bytes of the tcgen05 block-scale-factor buffer for a rows x cols operand
+ * (one E8M0 byte per 32 columns; 128-row x 4-block chunks of 512 B). */
+int64_t moss_sf_bytes(int64_t rows, int64_t cols);
+
+/* K0: amax = max|x| over n elements (f32 bits, written with atomicMax after a
+ * stream-ordered memset of *amax to 0).  Non-finite elements set
+ * MOSS_FLAG_NONFINITE.  Replaces the max-reductions of quantize.py:95 / 149-151
+ * and autoscale.py:58 (jit_scale).  Reads x back to front so that the
+ * following quantizer finds the head of x still in L2. */
+int moss_amax(const void* x, int dtype, int64_t n, float* amax, uint32_t* flags, void* stream);
+
+/* K1: two-level MOSS quantization, quant_two_level(x, E4M3, CEIL_POW2, k2=32,
+ * k1=None) (quantize.py:127-173), of a rows x cols row-major tensor.
+ *   amax         device f32 from moss_amax (g = f32(amax/448), 0 -> 1.0)
+ *   codes        [rows, cols] E4M3 codes, blocks of 32 along cols   (nullable)
+ *   sf           block-scale layout for the GEMM, moss_sf_bytes(rows, cols) (nullable)
+ *   micro        [rows, cols/32] row-major E8M0 codes (the reference layout) (nullable)
+ *   codes_t      [cols, rows] codes of quant_two_level(x.T): blocks of 32 along
+ *                rows (the wgrad operand), same g                  (nullable)
+ *   sf_t, micro_t  scales of codes_t, layouts as above              (nullable)
+ *   g_out        device f32 global scale (nullable)
+ * cols % 32 == 0; if codes_t/sf_t/micro_t is given also rows % 32 == 0. */
+int moss_quant_mx2(const void* x, int dtype, int64_t rows, int64_t cols, const float* amax,
+                   uint8_t* codes, uint8_t* sf, uint8_t* micro,
+                   uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t,
+                   float* g_out, uint32_t* flags, void* stream);
+
+/* Per-tensor encode at a given scale: codes = e4m3(f32(x) / f32(scale))
+ * (train.py:113-118 _quantize_weight, quant_per_tensor quantize.py:92-98 when
+ * scale = f32(amax/448), rescale_interval autoscale.py:86-96).
+ *   scale        device f32 (nullable: then scale_host is used; if also
+ *                scale_from_amax != 0, *scale is an amax and the scale is
+ *                f32(amax/448), 0 -> 1.0)
+ *   codes        [rows, cols] (nullable), codes_t [cols, rows] (nullable)
+ *   scale_out    device f32 receiving the scale actually used (nullable)
+ *   n_saturated  device u32 counter of |x| > scale*448 (nullable)          */
+int moss_encode_scaled(const void* x, int dtype, int64_t rows, int64_t cols, const float* scale,
+                       float scale_host, int scale_from_amax, uint8_t* codes, uint8_t* codes_t,
+                       float* scale_out, uint32_t* n_saturated, uint32_t* flags, void* stream);
+
+/* K2: block-scaled MXFP8 GEMM on tcgen05 (kind::mxf8f6f4, E8M0 scales in TMEM,
+ * FP32 accumulate), the dataflow of gemm_mx_epilogue (gemm.py:115-129):
+ *   D[m, n] = (sum_k A[m,k] 2^(SFA[m,k/32]-127) B[n,k] 2^(SFB[n,k/32]-127)) * (*sA) * (*sB)
+ * A [M,K] and B [N,K] are K-major E4M3 codes; SFA/SFB in the block-scale
+ * layout (SFB == NULL means unit scales: the per-tensor weight side,
+ * PAPER.md:103).  D is [M, N] row-major (ldd elements), bf16 or f32;
+ * accumulate != 0 adds into D (f32 only).  K % 128 == 0, M, N >= 1.
+ * The reference returns (out_features, tokens): call with A = weights,
+ * B = activations for that orientation, or A = activations for torch's. */
+int moss_gemm_mxf8(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB,
+                   const float* sA, const float* sB, void* D, int d_dtype, int64_t ldd,
+                   int64_t M, int64_t N, int64_t K, int accumulate, void* stream);
+
+/* K3 hyper-parameters of one AdamW step (optim.py:52-62, 78-106). */
+typedef struct {
+    float lr;         /* eta_t */
+    float beta1, beta2;
+    float eps;
+    float weight_decay;
+    float bc1, bc2;   /* 1 - beta1^t, 1 - beta2^t for the step being taken */
+    int decoupled;    /* 1 = AdamW (decay on the old weight), 0 = L2 into g */
+} moss_adam_params;
+
+/* K3: fused AdamW + automatic scaling + FP8 weight copy
+ * (adamw_step optim.py:78-106, then _quantize_weight train.py:113-118 at the
+ * advanced scale s_{t+1} = s_t + eta/448, autoscale.py:71-79).
+ * w, m, v   f32 [rows, cols] updated in place; g f32 or bf16.
+ * enc_scale f32(s_{t+1}) used for w_fp8 = e4m3(w'/enc_scale) (nullable outputs).
+ * w_fp8_t   [cols, rows] transposed codes for dgrad (nullable).
+ * w_amax    device f32 max|w'| (nullable; memset by the call) — rescale input.
+ * n_saturated  device u32 count of |w'| > enc_scale*448 (nullable).
+ * Elements whose gradient is non-finite are left untouched and set
+ * MOSS_FLAG_GRAD_NONFINITE (the reference raises before mutating). */
+int moss_adamw_fp8(float* w, const void* g, int g_dtype, float* m, float* v, int64_t rows, int64_t cols,
+                   const moss_adam_params* p, float enc_scale, uint8_t* w_fp8, uint8_t* w_fp8_t,
+                   float* w_amax, uint32_t* n_saturated, uint32_t* flags, void* stream);
+
+/* Human-readable status. */
+const char* moss_strerror(int status);
+
+/* Library ABI version (major*100 + minor). */
+int moss_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOSS_B200_H */

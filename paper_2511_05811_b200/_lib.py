@@ -1,0 +1,162 @@
+"""ctypes binding of the C ABI in include/moss_b200.h.
+
+There is deliberately no CPU fallback: if the in-tree library is missing or
+CUDA is unavailable, every entry point raises.  PyTorch provides device
+memory and the current stream; the arithmetic is all in libmoss_b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from . import errors
+from .build import LIB
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I = ctypes.c_int
+_F = ctypes.c_float
+
+MOSS_F32 = 0
+MOSS_BF16 = 1
+
+
+class AdamParams(ctypes.Structure):
+    _fields_ = [("lr", _F), ("beta1", _F), ("beta2", _F), ("eps", _F), ("weight_decay", _F),
+                ("bc1", _F), ("bc2", _F), ("decoupled", _I)]
+
+
+_SIGS = {
+    "moss_version": (_I, []),
+    "moss_strerror": (ctypes.c_char_p, [_I]),
+    "moss_sf_bytes": (_I64, [_I64, _I64]),
+    "moss_amax": (_I, [_P, _I, _I64, _P, _P, _P]),
+    "moss_quant_mx2": (_I, [_P, _I, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "moss_encode_scaled": (_I, [_P, _I, _I64, _I64, _P, _F, _I, _P, _P, _P, _P, _P, _P]),
+    "moss_gemm_mxf8": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _I, _P]),
+    "moss_adamw_fp8": (_I, [_P, _P, _I, _P, _P, _I64, _I64, ctypes.POINTER(AdamParams), _F, _P, _P, _P,
+                            _P, _P, _P]),
+}
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load (building first if needed) the sm_100a library; raise if impossible."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB):
+        from .build import build
+        try:
+            build()
+        except Exception as e:  # pragma: no cover - environment failure
+            raise errors.CudaError(f"libmoss_b200.so missing and build failed: {e}") from e
+    handle = ctypes.CDLL(LIB)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(handle, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = handle
+    return _lib
+
+
+_STATUS_EXC = {
+    1: errors.InvalidShapeError,
+    2: errors.InvalidValueError,
+    3: errors.InvalidArgumentError,
+    4: errors.E8m0RangeError,
+    5: errors.CudaError,
+    6: errors.InvalidArgumentError,
+}
+
+
+def check(status: int, what: str) -> None:
+    if status:
+        msg = lib().moss_strerror(status).decode()
+        raise _STATUS_EXC.get(status, errors.MossqError)(f"{what}: {msg}")
+
+
+def require_cuda(t: torch.Tensor, name: str) -> None:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise errors.InvalidArgumentError(f"{name} must be a CUDA tensor")
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return MOSS_BF16
+    if t.dtype == torch.float32:
+        return MOSS_F32
+    raise errors.InvalidArgumentError(f"unsupported dtype {t.dtype} (bf16 or f32)")
+
+
+def sf_bytes(rows: int, cols: int) -> int:
+    return int(lib().moss_sf_bytes(rows, cols))
+
+
+class FlagWord:
+    """A device u32 flag word (MOSS_FLAG_*) shared by a group of launches."""
+
+    def __init__(self, device=None):
+        self.t = torch.zeros(1, dtype=torch.int32, device=device or "cuda")
+
+    @property
+    def ptr(self) -> int:
+        return self.t.data_ptr()
+
+    def raise_if_set(self, where: str = "") -> None:
+        errors.raise_for_flags(int(self.t.item()), where)
+
+    def reset(self) -> None:
+        self.t.zero_()
+
+
+# ---------------------------------------------------------------- thin launchers
+def amax(x: torch.Tensor, out: torch.Tensor, flags: FlagWord) -> None:
+    check(lib().moss_amax(x.data_ptr(), dtype_code(x), x.numel(), out.data_ptr(), flags.ptr, stream()),
+          "moss_amax")
+
+
+def quant_mx2(x2d: torch.Tensor, amax_t: torch.Tensor, flags: FlagWord, *, codes=None, sf=None, micro=None,
+              codes_t=None, sf_t=None, micro_t=None, g_out=None) -> None:
+    rows, cols = x2d.shape
+    check(lib().moss_quant_mx2(x2d.data_ptr(), dtype_code(x2d), rows, cols, amax_t.data_ptr(), ptr(codes), ptr(sf),
+                               ptr(micro), ptr(codes_t), ptr(sf_t), ptr(micro_t), ptr(g_out), flags.ptr, stream()),
+          "moss_quant_mx2")
+
+
+def encode_scaled(x2d: torch.Tensor, flags: FlagWord, *, scale_t=None, scale_host: float = 0.0,
+                  from_amax: bool = False, codes=None, codes_t=None, scale_out=None, n_saturated=None) -> None:
+    rows, cols = x2d.shape
+    check(lib().moss_encode_scaled(x2d.data_ptr(), dtype_code(x2d), rows, cols, ptr(scale_t), float(scale_host),
+                                   int(from_amax), ptr(codes), ptr(codes_t), ptr(scale_out), ptr(n_saturated),
+                                   flags.ptr, stream()),
+          "moss_encode_scaled")
+
+
+def gemm(a, sfa, b, sfb, s_a, s_b, d, *, accumulate: bool = False) -> None:
+    m, k = a.shape
+    n = b.shape[0]
+    check(lib().moss_gemm_mxf8(a.data_ptr(), sfa.data_ptr(), b.data_ptr(), ptr(sfb), s_a.data_ptr(),
+                               s_b.data_ptr(), d.data_ptr(), dtype_code(d), d.stride(0), m, n, k,
+                               int(accumulate), stream()),
+          "moss_gemm_mxf8")
+
+
+def adamw_fp8(w, g, m, v, rows: int, cols: int, params: AdamParams, enc_scale: float, flags: FlagWord, *,
+              w_fp8=None, w_fp8_t=None, w_amax=None, n_saturated=None) -> None:
+    check(lib().moss_adamw_fp8(w.data_ptr(), g.data_ptr(), dtype_code(g), m.data_ptr(), v.data_ptr(), rows, cols,
+                               ctypes.byref(params), float(enc_scale), ptr(w_fp8), ptr(w_fp8_t), ptr(w_amax),
+                               ptr(n_saturated), flags.ptr, stream()),
+          "moss_adamw_fp8")
