@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""MOSS FP8 training-step benchmark (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], as a training step):
+  the five Llama-7B linear shapes of one decoder layer (QKV 4096->12288,
+  O 4096->4096, gate/up 4096->2x11008 fused, down 11008->4096) at M = 8192
+  tokens per GPU, through the public API (MossLinear + MossAdamW):
+  forward + backward with every input and gradient two-level quantized
+  (row- and column-wise) and every GEMM an FP8 tcgen05 block-scaled GEMM
+  (fwd, dgrad, wgrad), then the fused AdamW + autoscale + FP8 weight copy.
+  N > 1: data parallel, per-rank batch fixed (weak scaling), FP32 gradients
+  all-reduced over NCCL in buckets overlapped with backward.
+
+metric/unit: BASELINE.json's metric; value = whole-job GEMM FLOPs per second
+  (6 * tokens * sum(N*K) per step / step time, all ranks), TFLOP/s.
+e2e: the same step with the input copied from pinned host memory and the loss
+  read back to the host every step.
+roofline: the dominant kernel (the GEMM), FLOPs per launch / CUDA-event
+  duration per launch over the timed region, vs 2x the measured dense bf16
+  peak (MEASURED_PEAKS.json; fp8 dense = 2x bf16 on B200).
+cpu_baseline / --impl reference: the CPU oracle port (oracle/numpy_ref, the
+  reference's own numpy dataflow) timed on a bounded sample on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP8 GEMM TFLOP/s, quantize GB/s; 7B-shape train tokens/s at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--tokens", type=int, default=8192)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+def cpu_linear_step(tokens: int, d_in: int, d_out: int, seed: int = 0) -> float:
+    """One MOSS linear fwd + dgrad + wgrad + AdamW/autoscale step through the
+    CPU oracle (the reference's numpy dataflow: per-32-block float64 GEMMs,
+    gemm.py:115-129; float64 AdamW, optim.py:78-106).  Returns seconds."""
+    import numpy as np
+
+    from oracle import numpy_ref as R
+
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((tokens, d_in)).astype(np.float32)
+    w = rng.standard_normal((d_out, d_in)) * 0.02
+    dy = (rng.standard_normal((tokens, d_out)) * 1e-3).astype(np.float32)
+    st = R.adam_init(w.shape, eta=3e-4, weight_decay=0.1)
+    sched = R.Schedule(s_t=R.jit_scale(w))
+    t0 = time.perf_counter()
+    wc, _ = R.encode_weight(w, sched.s_t)                       # train.py:168
+    qx = R.quant_two_level(x)                                   # train.py:171
+    R.gemm_mx_epilogue(wc, sched.s_t, qx)                        # fwd
+    qdy = R.quant_two_level(dy)
+    R.gemm_mx_epilogue(np.ascontiguousarray(wc.T), sched.s_t, qdy)   # dgrad
+    qdy_t = R.quant_two_level(np.ascontiguousarray(dy.T))
+    qx_t = R.quant_two_level(np.ascontiguousarray(x.T))
+    a = R.dequantize_two_level(qdy_t)
+    b = R.fp8_decode(qx_t.codes).astype(np.float64)
+    ss = R.e8m0_decode(qx_t.micro_codes).astype(np.float64)
+    dw = np.zeros((d_out, d_in))
+    for blk in range(tokens // 32):                             # wgrad, same block dataflow
+        sl = slice(blk * 32, (blk + 1) * 32)
+        dw += (a[:, sl] @ b[:, sl].T) * ss[None, :, blk]
+    dw *= qx_t.global_scale
+    w, _ = R.adamw_step(w, dw, st)                              # optim.py:78-106
+    R.advance(sched, 3e-4)                                      # autoscale.py:71-79
+    return time.perf_counter() - t0
+
+
+def cpu_sample(tokens: int, d: int, reps: int = 1) -> dict:
+    secs = min(cpu_linear_step(tokens, d, d, seed=r) for r in range(reps))
+    flops = 6.0 * tokens * d * d
+    return {"value": flops / secs / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"one MOSS linear fwd+dgrad+wgrad+AdamW step, tokens={tokens}, {d}x{d}, oracle/numpy_ref "
+                      f"(reference numpy dataflow, float64 block GEMMs), {secs:.2f} s",
+            "seconds": secs}
+
+
+def run_reference(args, rank: int) -> None:
+    if rank != 0:
+        return
+    tokens, d = 256, 2048
+    for _ in range(args.warmup):
+        cpu_linear_step(tokens, d, d)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        cpu_linear_step(tokens, d, d, seed=i)
+    secs = (time.perf_counter() - t0) / args.steps
+    value = 6.0 * tokens * d * d / secs / 1e12
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (reference numpy)", "data": "synthetic",
+            "config": {"workload": "MOSS FP8 linear training step (reference CPU dataflow sample)",
+                       "tokens": tokens, "shape": [d, d]},
+            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"per step: one MOSS linear fwd+dgrad+wgrad+AdamW, tokens={tokens}, "
+                                       f"{d}x{d}, oracle/numpy_ref"},
+            "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self) -> dict:
+        rows = [r for r in self.rows if r[0] == str(self.idx)] or self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ GPU arm
+def main() -> None:
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    from paper_2511_05811_b200 import _lib
+    from paper_2511_05811_b200.dist import GradBuckets
+    from paper_2511_05811_b200.nn import MossAdamW
+    from paper_2511_05811_b200.workloads import LayerStack
+
+    dev = torch.device("cuda", local)
+    torch.manual_seed(1234 + rank)
+    model = LayerStack(device=dev)
+    opt = MossAdamW(model, lr=3e-4, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1)
+    buckets = GradBuckets(model, bucket_mb=64) if world > 1 else None
+    if buckets is not None:
+        opt.grad_scale = buckets.grad_scale
+    T = args.tokens
+    x = torch.randn(T, model.d, device=dev, dtype=torch.bfloat16)
+    flops_step = float(model.gemm_flops_per_token()) * T
+
+    def step(xin):
+        if buckets is not None:
+            buckets.reset()
+        else:
+            opt.zero_grad()
+        loss = model(xin)
+        loss.backward()
+        if buckets is not None:
+            buckets.finish()
+        opt.step()
+        return loss
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        step(x)
+    opt.check("warmup")
+    barrier()
+
+    # ---- timed region: inputs resident in HBM; working set per step (~3 GB) >> L2
+    s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        _lib.INSTR.start(timing=True)
+        s_ev.record()
+        for _ in range(args.steps):
+            loss = step(x)
+        e_ev.record()
+        torch.cuda.synchronize()
+        _lib.INSTR.stop()
+    barrier()
+    ms = s_ev.elapsed_time(e_ev) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    opt.check("timed region")
+    kern = _lib.INSTR.summary()
+    launches = _lib.INSTR.launches // args.steps
+
+    # ---- e2e: input from pinned host memory, loss read back every step
+    e2e = None
+    if not args.no_e2e:
+        x_host = x.cpu().pin_memory()
+        loss_host = torch.empty(1, dtype=torch.float32).pin_memory()
+        barrier()
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record()
+        for _ in range(args.steps):
+            xin = x_host.to(dev, non_blocking=True)
+            loss = step(xin)
+            loss_host.copy_(loss.detach().view(1), non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        e2.record()
+        torch.cuda.synchronize()
+        ms_e2e = s2.elapsed_time(e2) / args.steps
+        if world > 1:
+            t = torch.tensor([ms_e2e], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        e2e = {"value": world * flops_step / (ms_e2e / 1e3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": x_host.numel() * x_host.element_size(), "d2h_bytes_per_step": 4,
+               "ms_per_step": ms_e2e}
+
+    if rank != 0:
+        dist.destroy_process_group() if world > 1 else None
+        return
+
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    bf16_sus = peaks.get("bf16_tflops_sustained", 1400.0)
+    bf16_burst = peaks.get("bf16_tflops", 1590.0)
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    fp8_peak = 2.0 * bf16_sus
+    g = kern.get("gemm", {"launches": 0, "ms": 1e-9, "work": 0})
+    gemm_tflops = g["work"] / (g["ms"] / 1e3) / 1e12 if g["launches"] else 0.0
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")))
+        traffic = prof.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    def rate(kind):
+        d = kern.get(kind)
+        if not d or not d["launches"]:
+            return None
+        return {"launches_per_step": d["launches"] // args.steps, "ms_per_step": d["ms"] / args.steps,
+                "achieved_gbs": d["work"] / (d["ms"] / 1e3) / 1e9,
+                "frac_of_hbm": d["work"] / (d["ms"] / 1e3) / 1e9 / hbm}
+
+    total_kernel_ms = sum(d["ms"] for d in kern.values()) / args.steps
+    line = {
+        "metric": METRIC,
+        "value": world * flops_step / (ms / 1e3) / 1e12,
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(3, args.warmup),
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "e4m3 x e4m3 -> fp32 accumulate (MXFP8, E8M0 block scales); bf16 activations; fp32 master/optimizer",
+        "data": "synthetic (randn bf16 activations, N(0,0.02^2) weights, random init)",
+        "config": {"workload": "configs[1]: MOSS quantize + MXFP8 fwd/dgrad/wgrad GEMMs over the Llama-7B linear "
+                               "shapes (QKV 4096->12288, O 4096->4096, gate/up 4096->2x11008, down 11008->4096) "
+                               "+ fused AdamW/autoscale/FP8-copy, as one training step",
+                   "tokens_per_gpu": T, "global_batch_tokens": T * world,
+                   "parallelism": f"dp{world}" + (" (NCCL bucketed fp32 grad all-reduce)" if world > 1 else ""),
+                   "gemm_flops_per_step_per_gpu": flops_step,
+                   "l2": "not flushed: per-step working set ~3 GB >> 126 MB L2"},
+        "tokens_per_s": world * T / (ms / 1e3),
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "roofline": {"bound": "tensor", "kernel": "moss::gemm_mxf8_kernel (tcgen05 mxf8f6f4 block_scale)",
+                     "achieved": gemm_tflops, "peak": fp8_peak, "unit": "TFLOP/s", "frac": gemm_tflops / fp8_peak,
+                     "peak_source": "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (fp8 dense = 2x bf16)",
+                     "frac_of_burst": gemm_tflops / (2.0 * bf16_burst), "traffic": traffic,
+                     "share_of_step": (g["ms"] / args.steps) / ms if g["launches"] else None},
+        "kernels": {"quantize": rate("quant"), "amax": rate("amax"), "adamw_fp8": rate("adamw"),
+                    "gemm_ms_per_step": g["ms"] / args.steps, "all_kernels_ms_per_step": total_kernel_ms},
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_sample(1024, 4096)
+        line["cpu_baseline"].pop("seconds", None)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

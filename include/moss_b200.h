@@ -101,6 +101,7 @@ typedef struct {
     float weight_decay;
     float bc1, bc2;   /* 1 - beta1^t, 1 - beta2^t for the step being taken */
     int decoupled;    /* 1 = AdamW (decay on the old weight), 0 = L2 into g */
+    float grad_scale; /* g is multiplied by this first (DP averaging, grad accumulation); 1 = none */
 } moss_adam_params;
 
 /* K3: fused AdamW + automatic scaling + FP8 weight copy

@@ -26,7 +26,7 @@ MOSS_BF16 = 1
 
 class AdamParams(ctypes.Structure):
     _fields_ = [("lr", _F), ("beta1", _F), ("beta2", _F), ("eps", _F), ("weight_decay", _F),
-                ("bc1", _F), ("bc2", _F), ("decoupled", _I)]
+                ("bc1", _F), ("bc2", _F), ("decoupled", _I), ("grad_scale", _F)]
 
 
 _SIGS = {
@@ -122,41 +122,106 @@ class FlagWord:
         self.t.zero_()
 
 
+# ---------------------------------------------------------------- live instrumentation
+class Instrument:
+    """Counts our kernel launches and (optionally) brackets each with CUDA
+    events on the launching stream, recording the algorithmic work of the
+    launch (FLOPs for GEMMs, bytes for the HBM-bound kernels).  bench.py
+    turns this into per-kernel roofline numbers over its timed region."""
+
+    def __init__(self):
+        self.active = False
+        self.timing = False
+        self.launches = 0
+        self.records: list[tuple[str, float, torch.cuda.Event, torch.cuda.Event]] = []
+
+    def start(self, timing: bool = True) -> None:
+        self.active, self.timing, self.launches, self.records = True, timing, 0, []
+
+    def stop(self) -> None:
+        self.active = False
+
+    def summary(self) -> dict:
+        out: dict[str, dict] = {}
+        for kind, work, s, e in self.records:
+            d = out.setdefault(kind, {"launches": 0, "ms": 0.0, "work": 0.0})
+            d["launches"] += 1
+            d["ms"] += s.elapsed_time(e)
+            d["work"] += work
+        return out
+
+
+INSTR = Instrument()
+
+
+class _Span:
+    __slots__ = ("kind", "work", "s")
+
+    def __init__(self, kind: str, work: float, kernels: int = 1):
+        self.kind, self.work, self.s = kind, work, None
+        if INSTR.active:
+            INSTR.launches += kernels
+            if INSTR.timing:
+                self.s = torch.cuda.Event(enable_timing=True)
+                self.s.record()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        if self.s is not None and exc[0] is None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            INSTR.records.append((self.kind, self.work, self.s, e))
+        return False
+
+
 # ---------------------------------------------------------------- thin launchers
 def amax(x: torch.Tensor, out: torch.Tensor, flags: FlagWord) -> None:
-    check(lib().moss_amax(x.data_ptr(), dtype_code(x), x.numel(), out.data_ptr(), flags.ptr, stream()),
-          "moss_amax")
+    with _Span("amax", x.numel() * x.element_size()):
+        check(lib().moss_amax(x.data_ptr(), dtype_code(x), x.numel(), out.data_ptr(), flags.ptr, stream()),
+              "moss_amax")
 
 
 def quant_mx2(x2d: torch.Tensor, amax_t: torch.Tensor, flags: FlagWord, *, codes=None, sf=None, micro=None,
               codes_t=None, sf_t=None, micro_t=None, g_out=None) -> None:
     rows, cols = x2d.shape
-    check(lib().moss_quant_mx2(x2d.data_ptr(), dtype_code(x2d), rows, cols, amax_t.data_ptr(), ptr(codes), ptr(sf),
-                               ptr(micro), ptr(codes_t), ptr(sf_t), ptr(micro_t), ptr(g_out), flags.ptr, stream()),
-          "moss_quant_mx2")
+    n = rows * cols
+    out_b = (n + n / 32) * ((codes is not None) + (codes_t is not None))
+    with _Span("quant", n * x2d.element_size() + out_b):
+        check(lib().moss_quant_mx2(x2d.data_ptr(), dtype_code(x2d), rows, cols, amax_t.data_ptr(), ptr(codes),
+                                   ptr(sf), ptr(micro), ptr(codes_t), ptr(sf_t), ptr(micro_t), ptr(g_out), flags.ptr,
+                                   stream()),
+              "moss_quant_mx2")
 
 
 def encode_scaled(x2d: torch.Tensor, flags: FlagWord, *, scale_t=None, scale_host: float = 0.0,
                   from_amax: bool = False, codes=None, codes_t=None, scale_out=None, n_saturated=None) -> None:
     rows, cols = x2d.shape
-    check(lib().moss_encode_scaled(x2d.data_ptr(), dtype_code(x2d), rows, cols, ptr(scale_t), float(scale_host),
-                                   int(from_amax), ptr(codes), ptr(codes_t), ptr(scale_out), ptr(n_saturated),
-                                   flags.ptr, stream()),
-          "moss_encode_scaled")
+    n = rows * cols
+    with _Span("encode", n * x2d.element_size() + n * ((codes is not None) + (codes_t is not None))):
+        check(lib().moss_encode_scaled(x2d.data_ptr(), dtype_code(x2d), rows, cols, ptr(scale_t), float(scale_host),
+                                       int(from_amax), ptr(codes), ptr(codes_t), ptr(scale_out), ptr(n_saturated),
+                                       flags.ptr, stream()),
+              "moss_encode_scaled")
 
 
 def gemm(a, sfa, b, sfb, s_a, s_b, d, *, accumulate: bool = False) -> None:
     m, k = a.shape
     n = b.shape[0]
-    check(lib().moss_gemm_mxf8(a.data_ptr(), sfa.data_ptr(), b.data_ptr(), ptr(sfb), s_a.data_ptr(),
-                               s_b.data_ptr(), d.data_ptr(), dtype_code(d), d.stride(0), m, n, k,
-                               int(accumulate), stream()),
-          "moss_gemm_mxf8")
+    with _Span("gemm", 2.0 * m * n * k):
+        check(lib().moss_gemm_mxf8(a.data_ptr(), sfa.data_ptr(), b.data_ptr(), ptr(sfb), s_a.data_ptr(),
+                                   s_b.data_ptr(), d.data_ptr(), dtype_code(d), d.stride(0), m, n, k,
+                                   int(accumulate), stream()),
+              "moss_gemm_mxf8")
 
 
 def adamw_fp8(w, g, m, v, rows: int, cols: int, params: AdamParams, enc_scale: float, flags: FlagWord, *,
               w_fp8=None, w_fp8_t=None, w_amax=None, n_saturated=None) -> None:
-    check(lib().moss_adamw_fp8(w.data_ptr(), g.data_ptr(), dtype_code(g), m.data_ptr(), v.data_ptr(), rows, cols,
-                               ctypes.byref(params), float(enc_scale), ptr(w_fp8), ptr(w_fp8_t), ptr(w_amax),
-                               ptr(n_saturated), flags.ptr, stream()),
-          "moss_adamw_fp8")
+    n = rows * cols
+    nbytes = n * (4 + g.element_size() + 8) + n * 12 + n * ((w_fp8 is not None) + (w_fp8_t is not None))
+    with _Span("adamw", nbytes):
+        check(lib().moss_adamw_fp8(w.data_ptr(), g.data_ptr(), dtype_code(g), m.data_ptr(), v.data_ptr(), rows,
+                                   cols, ctypes.byref(params), float(enc_scale), ptr(w_fp8), ptr(w_fp8_t),
+                                   ptr(w_amax), ptr(n_saturated), flags.ptr, stream()),
+              "moss_adamw_fp8")

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) adamw_fp8_kernel(float* __restrict__ w, c
             Vec8<float>::load(v + off, vv);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                float gj = gv[j];
+                float gj = gv[j] * p.grad_scale;
                 if (nonfinite(gj)) {  // leave this element untouched; host raises
                     bad = true;
                     continue;

@@ -49,10 +49,11 @@ def init_state(shape, *, beta1: float = 0.9, beta2: float = 0.95, eta: float = 1
 
 
 def adam_params(lr: float, beta1: float, beta2: float, eps: float, weight_decay: float, t: int,
-                decoupled: bool) -> _lib.AdamParams:
+                decoupled: bool, grad_scale: float = 1.0) -> _lib.AdamParams:
     """Kernel hyper-parameters for step number t (>= 1); bias corrections in f64."""
     return _lib.AdamParams(lr=lr, beta1=beta1, beta2=beta2, eps=eps, weight_decay=weight_decay,
-                           bc1=1.0 - beta1 ** t, bc2=1.0 - beta2 ** t, decoupled=int(decoupled))
+                           bc1=1.0 - beta1 ** t, bc2=1.0 - beta2 ** t, decoupled=int(decoupled),
+                           grad_scale=grad_scale)
 
 
 def _as_2d(t: torch.Tensor) -> tuple[int, int]:

@@ -1,0 +1,47 @@
+"""Benchmark / parity workloads built only from the public training API.
+
+``LayerStack`` is BASELINE config 2 as a training step: the five Llama-7B
+linear shapes of one decoder layer (QKV 4096->12288, O 4096->4096,
+gate/up 4096->2x11008 fused, down 11008->4096) at M tokens, chained with
+cheap bf16 glue so that every linear sees a real forward input and a real
+backward gradient:
+
+    qkv = QKV(x); a = q + k + v              (stand-in for attention mixing)
+    r = x + O(a); h = silu(gate(r)) * up(r); y = down(h); loss = mean(y^2)
+
+One step = forward + backward (FP8 fwd/dgrad/wgrad for every linear, each
+input and gradient two-level quantized row- and column-wise) + MossAdamW
+(fused update + autoscale + FP8 weight copy).  GEMM FLOPs per step:
+6 * M * sum(N*K) = 6 * M * 202.4M.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.nn.functional as F
+from torch import nn
+
+from .nn import MossLinear
+
+LLAMA7B_SHAPES = {"qkv": (4096, 12288), "o": (4096, 4096), "gate_up": (4096, 22016), "down": (11008, 4096)}
+
+
+class LayerStack(nn.Module):
+    def __init__(self, d_model: int = 4096, d_ffn: int = 11008, device="cuda", interval: int = 500):
+        super().__init__()
+        self.d, self.f = d_model, d_ffn
+        self.qkv = MossLinear(d_model, 3 * d_model, device=device, interval=interval)
+        self.o = MossLinear(d_model, d_model, device=device, interval=interval)
+        self.gate_up = MossLinear(d_model, 2 * d_ffn, device=device, interval=interval)
+        self.down = MossLinear(d_ffn, d_model, device=device, interval=interval)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        q, k, v = self.qkv(x).split(self.d, dim=-1)
+        a = q + k + v
+        r = x + self.o(a)
+        g, u = self.gate_up(r).split(self.f, dim=-1)
+        y = self.down(F.silu(g) * u)
+        return (y.float() ** 2).mean()
+
+    def gemm_flops_per_token(self) -> int:
+        return 6 * sum(m.in_features * m.out_features for m in (self.qkv, self.o, self.gate_up, self.down))
