@@ -19,6 +19,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "host_utils.cuh"
 
 namespace moss {
 
@@ -222,33 +223,9 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 }
 
 // ------------------------------------------------------------------ host side
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn get_encode_fn() {
-    static EncodeTiledFn fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeTiledFn>(p);
-    }
-    return fn;
-}
-
 // K-major uint8 operand [rows, k]: box = 128 B of K x box_rows rows, 128B swizzle.
 static bool make_kmajor_map(CUtensorMap* map, const void* ptr, int64_t rows, int64_t k, int box_rows) {
-    EncodeTiledFn enc = get_encode_fn();
-    if (!enc) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)k};
-    cuuint32_t box[2] = {128u, (cuuint32_t)box_rows};
-    cuuint32_t estr[2] = {1u, 1u};
-    return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return make_tmap_2d(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ptr, rows, k, 128, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 template <int BN, int STAGES, bool OUT_BF16>
@@ -265,12 +242,7 @@ static int launch_gemm_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B,
     }
     CUtensorMap ta, tb;
     if (!make_kmajor_map(&ta, A, M, K, G_BM) || !make_kmajor_map(&tb, B, N, K, BN)) return MOSS_ERR_CUDA;
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = sm_count();
     const int64_t tiles = (M / G_BM) * (N / BN);
     const int grid = (int)std::min<int64_t>(tiles, sms);
     kern<<<grid, G_THREADS, L::SMEM, st>>>(ta, tb, SFA, SFB, sA, sB, D, ldd, (int)M, (int)N, (int)K, accumulate);

@@ -155,6 +155,57 @@ def test_two_level_row_and_col_bit_exact_at_scale(c_oracle, shape, dist, dtype):
         assert np.array_equal(unswizzle_sf(host(op.sf_t), cols, rows // 32), micro_t)
 
 
+def _bf16_sweep_tensor(amax_bits: int, rng) -> np.ndarray:
+    """[rows, 256] f32 (exact bf16 values): block 0 holds the tensor max A;
+    every block k holds a block max A*2^-j (varied exponent) and up to 31
+    bf16 patterns not exceeding it — all 65536 patterns appear at least once."""
+    A = np.uint32(amax_bits << 16).view(np.float32)
+    pats = (np.arange(1 << 16, dtype=np.uint32) << 16).view(np.float32)
+    pats = pats[np.isfinite(pats)]
+    blocks = []
+    for j in range(0, 40, 3):
+        bm = np.float32(A * np.float32(2.0 ** -j))
+        bm = (np.float32(bm).view(np.uint32) & 0xFFFF0000).view(np.float32)   # keep it a bf16 value
+        if not np.isfinite(bm) or bm == 0:
+            continue
+        ok = pats[np.abs(pats) <= bm]
+        if ok.size == 0:
+            continue
+        n_blk = -(-ok.size // 31)
+        body = np.zeros(n_blk * 31, np.float32)
+        body[:ok.size] = ok
+        blk = np.concatenate([np.full((n_blk, 1), bm, np.float32), body.reshape(n_blk, 31)], axis=1)
+        blocks.append(blk.reshape(-1))
+    flat = np.concatenate(blocks)
+    flat[0] = A
+    pad = (-flat.size) % (32 * 256)
+    flat = np.concatenate([flat, np.zeros(pad, np.float32)])
+    return flat.reshape(-1, 256)
+
+
+@pytest.mark.slow
+def test_bf16_fast_division_exhaustive(c_oracle):
+    """The bf16 TMA quantizer divides with a per-block reciprocal + FMA
+    correction (common.cuh block_div); prove it equals IEEE division on every
+    bf16 input pattern for many global scales (random significands, the
+    all-ones significand, extreme exponents), row- and column-wise."""
+    rng = np.random.default_rng(11)
+    amaxes = [0x7F7F, 0x3FFF, 0x3F80, 0x0080, 0x0100, 0x43E0, 0x7F00, 0x1F7F]
+    amaxes += [int(v) for v in rng.integers(0x0080, 0x7F7F, 40)]
+    for ab in amaxes:
+        x = _bf16_sweep_tensor(ab, rng)
+        xt = cuda(x, torch.bfloat16)
+        assert np.array_equal(host(xt.float()), x)
+        op = quantize_mx2(xt, row=True, col=True, micro=True)
+        codes, micro, g, st = c_oracle.quant_two_level(x)
+        assert float(op.g.item()) == g, hex(ab)
+        assert np.array_equal(host(op.micro), micro), hex(ab)
+        assert np.array_equal(host(op.codes), codes), hex(ab)
+        codes_t, micro_t, _, _ = c_oracle.quant_two_level(np.ascontiguousarray(x.T))
+        assert np.array_equal(host(op.codes_t), codes_t), hex(ab)
+        assert np.array_equal(host(op.micro_t), micro_t), hex(ab)
+
+
 def test_two_level_properties_full_size():
     """Size-independent properties at the 8192 x 11008 down-proj shape."""
     torch.manual_seed(0)
