@@ -228,8 +228,10 @@ def main() -> None:
     with ClockSampler(local) as clocks:
         _lib.INSTR.start(timing=True)
         s_ev.record()
+        h0 = time.perf_counter()
         for _ in range(args.steps):
             loss = step(x)
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
         e_ev.record()
         torch.cuda.synchronize()
         _lib.INSTR.stop()
@@ -327,7 +329,8 @@ def main() -> None:
                      "frac_of_burst": gemm_tflops / (2.0 * bf16_burst), "traffic": traffic,
                      "share_of_step": (g["ms"] / args.steps) / ms if g["launches"] else None},
         "kernels": {"quantize": rate("quant"), "amax": rate("amax"), "adamw_fp8": rate("adamw"),
-                    "gemm_ms_per_step": g["ms"] / args.steps, "all_kernels_ms_per_step": total_kernel_ms},
+                    "gemm_ms_per_step": g["ms"] / args.steps, "all_kernels_ms_per_step": total_kernel_ms,
+                    "host_issue_ms_per_step": host_ms},
         "e2e": e2e,
     }
     if not args.no_cpu_baseline and world == 1:

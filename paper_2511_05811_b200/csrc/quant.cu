@@ -240,10 +240,7 @@ __global__ void __launch_bounds__(256) quant_mx2_tma_kernel(const __grid_constan
             const uint32_t code = block_scale(bm, g, eff, rerr);
             const BlockDiv d = make_block_div(eff);
             uint32_t w[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                w[q] = e4m3x4(block_div(d, v[4 * q]), block_div(d, v[4 * q + 1]), block_div(d, v[4 * q + 2]),
-                              block_div(d, v[4 * q + 3]));
+            encode_block32(v, d, w);
             const int64_t row = r0 + r;
             const int kbg = (c0 >> 5) + kb;
             if (codes) {
@@ -267,10 +264,7 @@ __global__ void __launch_bounds__(256) quant_mx2_tma_kernel(const __grid_constan
             const uint32_t code = block_scale(bm, g, eff, rerr);
             const BlockDiv d = make_block_div(eff);
             uint32_t w[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                w[q] = e4m3x4(block_div(d, v[4 * q]), block_div(d, v[4 * q + 1]), block_div(d, v[4 * q + 2]),
-                              block_div(d, v[4 * q + 3]));
+            encode_block32(v, d, w);
             const int64_t col = c0 + c;
             if (codes_t) {
                 uint4* dst = reinterpret_cast<uint4*>(codes_t + col * rows + r0);
