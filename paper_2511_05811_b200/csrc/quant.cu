@@ -159,130 +159,6 @@ __global__ void __launch_bounds__(256) quant_mx2_kernel(const T* __restrict__ x,
     if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(flags, MOSS_FLAG_NONFINITE);
 }
 
-// ------------------------------------------------------------------ K1 fast path (bf16)
-// Persistent, TMA-fed: 32 x 256 bf16 tiles (16 KB) land in shared memory in
-// the TMA 128B-swizzle layout through a QF_STAGES-deep mbarrier ring; each of
-// the 256 threads then owns exactly one 32-element block in each pass (row
-// pass: (row, k-block); column pass: one column of the 32-row block), so the
-// per-block scale math runs once per block and every element costs one
-// max, one exact block_div and half a cvt.  Non-finite inputs are detected
-// by K0 (amax), not here.
-constexpr int QF_ROWS = 32;
-constexpr int QF_COLS = 256;
-constexpr int QF_STAGES = 3;
-constexpr int QF_TILE = QF_ROWS * QF_COLS * 2;
-
-// byte offset of element (r, c) inside a tile: four 64-column TMA boxes of
-// 32 rows x 128 B, 16 B chunks XOR-swizzled with the row (SWIZZLE_128B)
-__device__ __forceinline__ uint32_t qf_off(int r, int c) {
-    return (uint32_t)((c >> 6) * 4096 + r * 128 + ((((c >> 3) & 7) ^ (r & 7)) << 4) + ((c & 7) << 1));
-}
-
-__device__ __forceinline__ void bf16x8(uint4 u, float* v) {
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        v[2 * i] = __uint_as_float(w[i] << 16);
-        v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
-    }
-}
-
-template <bool ROW, bool COL>
-__global__ void __launch_bounds__(256) quant_mx2_tma_kernel(const __grid_constant__ CUtensorMap tmx, int rows,
-                                                            int cols, const float* __restrict__ amax_p,
-                                                            uint8_t* codes, uint8_t* sf, uint8_t* micro,
-                                                            uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t,
-                                                            float* g_out, uint32_t* flags) {
-    extern __shared__ uint8_t qsmem_raw[];
-    uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(qsmem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(tiles + QF_STAGES * QF_TILE);
-    const int tid = threadIdx.x;
-    const int ctiles = cols / QF_COLS;
-    const int ntiles = ctiles * (rows / QF_ROWS);
-    if (tid == 0) {
-        for (int s = 0; s < QF_STAGES; ++s) mbar_init(&full[s], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
-    auto issue = [&](int tile, int s) {
-        const int r0 = (tile / ctiles) * QF_ROWS, c0 = (tile % ctiles) * QF_COLS;
-        mbar_arrive_expect_tx(&full[s], QF_TILE);
-#pragma unroll
-        for (int b = 0; b < 4; ++b) tma_load_2d(tiles + s * QF_TILE + b * 4096, &tmx, &full[s], c0 + b * 64, r0);
-    };
-    if (tid == 0) {
-        for (int s = 0; s < QF_STAGES; ++s) {
-            const int tile = blockIdx.x + s * gridDim.x;
-            if (tile < ntiles) issue(tile, s);
-        }
-    }
-    const float g = global_scale_from_amax(*amax_p);
-    if (g_out && blockIdx.x == 0 && tid == 0) *g_out = g;
-    const int nb_row = cols >> 5, kch_row = (nb_row + 3) >> 2;
-    const int nb_t = rows >> 5, kch_t = (nb_t + 3) >> 2;
-    bool rerr = false;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int s = it % QF_STAGES;
-        mbar_wait(&full[s], (uint32_t)((it / QF_STAGES) & 1));
-        const uint8_t* T = tiles + s * QF_TILE;
-        const int r0 = (tile / ctiles) * QF_ROWS, c0 = (tile % ctiles) * QF_COLS;
-        if (ROW) {
-            const int r = tid & 31, kb = tid >> 5;
-            float v[32];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                bf16x8(*reinterpret_cast<const uint4*>(T + qf_off(r, kb * 32 + q * 8)), v + 8 * q);
-            float bm = 0.f;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) bm = fmaxf(bm, fabsf(v[j]));
-            float eff;
-            const uint32_t code = block_scale(bm, g, eff, rerr);
-            const BlockDiv d = make_block_div(eff);
-            uint32_t w[8];
-            encode_block32(v, d, w);
-            const int64_t row = r0 + r;
-            const int kbg = (c0 >> 5) + kb;
-            if (codes) {
-                uint4* dst = reinterpret_cast<uint4*>(codes + row * cols + c0 + kb * 32);
-                dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-                dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-            }
-            if (sf) sf[sf_offset(row, kbg, kch_row)] = (uint8_t)code;
-            if (micro) micro[row * nb_row + kbg] = (uint8_t)code;
-        }
-        if (COL) {
-            const int c = tid;
-            float v[32];
-#pragma unroll
-            for (int r = 0; r < 32; ++r)
-                v[r] = __uint_as_float((uint32_t)(*reinterpret_cast<const uint16_t*>(T + qf_off(r, c))) << 16);
-            float bm = 0.f;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) bm = fmaxf(bm, fabsf(v[j]));
-            float eff;
-            const uint32_t code = block_scale(bm, g, eff, rerr);
-            const BlockDiv d = make_block_div(eff);
-            uint32_t w[8];
-            encode_block32(v, d, w);
-            const int64_t col = c0 + c;
-            if (codes_t) {
-                uint4* dst = reinterpret_cast<uint4*>(codes_t + col * rows + r0);
-                dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-                dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-            }
-            if (sf_t) sf_t[sf_offset(col, r0 >> 5, kch_t)] = (uint8_t)code;
-            if (micro_t) micro_t[col * nb_t + (r0 >> 5)] = (uint8_t)code;
-        }
-        __syncthreads();  // every thread is done reading stage s
-        if (tid == 0) {
-            const int next = tile + QF_STAGES * gridDim.x;
-            if (next < ntiles) issue(next, s);
-        }
-    }
-    if (__any_sync(0xFFFFFFFFu, rerr) && (tid & 31) == 0) atomicOr(flags, MOSS_FLAG_E8M0_RANGE);
-}
-
 // ------------------------------------------------------------------ per-tensor encode
 template <typename T>
 __global__ void __launch_bounds__(256) encode_scaled_kernel(const T* __restrict__ x, int64_t rows, int64_t cols,
@@ -371,37 +247,15 @@ static void launch_quant_t(const T* x, int64_t rows, int64_t cols, const float* 
                                                                micro_t, g_out, flags);
 }
 
-static bool launch_quant_tma(const void* x, int64_t rows, int64_t cols, const float* amax, uint8_t* codes,
-                             uint8_t* sf, uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t,
-                             float* g_out, uint32_t* flags, cudaStream_t st) {
-    if (rows % QF_ROWS || cols % QF_COLS || rows > INT32_MAX || cols > INT32_MAX) return false;
-    CUtensorMap map;
-    if (!make_tmap_2d(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, rows, cols, 64, QF_ROWS,
-                      CU_TENSOR_MAP_SWIZZLE_128B))
-        return false;
-    const int smem = QF_STAGES * QF_TILE + 64 + 1024;
-    const bool row = codes || sf || micro;
-    const bool col = codes_t || sf_t || micro_t;
-    auto kern = row && col ? quant_mx2_tma_kernel<true, true>
-                           : (col ? quant_mx2_tma_kernel<false, true> : quant_mx2_tma_kernel<true, false>);
-    static bool attr[3] = {false, false, false};
-    const int ki = row && col ? 0 : (col ? 1 : 2);
-    if (!attr[ki]) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr[ki] = true;
-    }
-    const int64_t ntiles = (rows / QF_ROWS) * (cols / QF_COLS);
-    const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * 4);
-    kern<<<grid, 256, smem, st>>>(map, (int)rows, (int)cols, amax, codes, sf, micro, codes_t, sf_t, micro_t, g_out,
-                                  flags);
-    return true;
-}
+bool launch_quant_v3(const void* x, int64_t rows, int64_t cols, const float* amax, uint8_t* codes, uint8_t* sf,
+                     uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t, float* g_out,
+                     uint32_t* flags, cudaStream_t st);
 
 int launch_quant_mx2(const void* x, int dtype, int64_t rows, int64_t cols, const float* amax, uint8_t* codes,
                      uint8_t* sf, uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t, float* g_out,
                      uint32_t* flags, cudaStream_t st) {
     if (dtype == MOSS_BF16 &&
-        launch_quant_tma(x, rows, cols, amax, codes, sf, micro, codes_t, sf_t, micro_t, g_out, flags, st))
+        launch_quant_v3(x, rows, cols, amax, codes, sf, micro, codes_t, sf_t, micro_t, g_out, flags, st))
         return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
     if (dtype == MOSS_BF16)
         launch_quant_t((const __nv_bfloat16*)x, rows, cols, amax, codes, sf, micro, codes_t, sf_t, micro_t, g_out,

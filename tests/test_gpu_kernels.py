@@ -178,7 +178,7 @@ def _bf16_sweep_tensor(amax_bits: int, rng) -> np.ndarray:
         blocks.append(blk.reshape(-1))
     flat = np.concatenate(blocks)
     flat[0] = A
-    pad = (-flat.size) % (32 * 256)
+    pad = (-flat.size) % (128 * 256)          # rows % 128 == 0: exercises the TMA fast path
     flat = np.concatenate([flat, np.zeros(pad, np.float32)])
     return flat.reshape(-1, 256)
 
