@@ -17,6 +17,7 @@
 // Pipelines: STAGES-deep smem ring (full/empty mbarriers), one TMEM
 // accumulator (tmem_full/tmem_empty mbarriers).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "host_utils.cuh"
@@ -249,9 +250,26 @@ static int launch_gemm_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B,
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 
+int launch_gemm2(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
+                 const float* sB, void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
+                 cudaStream_t st);
+
+static int gemm_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MOSS_GEMM_VARIANT");   // "1" forces the 1-CTA kernel (A/B testing)
+        v = (e && e[0] == '1') ? 1 : 2;
+    }
+    return v;
+}
+
 int launch_gemm(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
                 const float* sB, void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
                 cudaStream_t st) {
+    if (gemm_variant() == 2) {
+        const int r = launch_gemm2(A, SFA, B, SFB, sA, sB, D, d_dtype, ldd, M, N, K, accumulate, st);
+        if (r >= 0) return r;
+    }
     const bool bn256 = (N % 256) == 0;
     if (d_dtype == MOSS_BF16) {
         return bn256 ? launch_gemm_t<256, 4, true>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)

@@ -298,9 +298,10 @@ def test_gemm_vs_f64_oracle_on_device_codes(mnk, out_dtype):
     assert float(np.max(np.abs(got - ref) / (mag + 1e-30))) <= (1e-5 if out_dtype == torch.float32 else 4e-3)
 
 
-def test_gemm_unit_and_real_scales_both_sides():
-    """Two-level operands on BOTH sides (wgrad-style) and accumulate=True."""
-    m, n, k = 384, 512, 2048
+@pytest.mark.parametrize("m,n,k", [(384, 512, 2048), (512, 768, 1024), (1024, 512, 4096)])
+def test_gemm_unit_and_real_scales_both_sides(m, n, k):
+    """Two-level operands on BOTH sides (wgrad-style) and accumulate=True
+    (1-CTA kernel for M % 256 != 0, CTA-pair kernel otherwise)."""
     torch.manual_seed(1)
     a = torch.randn(m, k, device="cuda") * torch.logspace(-3, 1, k, device="cuda")
     b = torch.randn(n, k, device="cuda")
@@ -311,6 +312,35 @@ def test_gemm_unit_and_real_scales_both_sides():
     ref = R.gemm_f64(R.dequantize_two_level(R.TwoLevel(host(qa.codes), float(qa.g.item()), host(qa.micro))),
                      R.dequantize_two_level(R.TwoLevel(host(qb.codes), float(qb.g.item()), host(qb.micro))))
     assert rel_frob(host(d) - host(acc), ref) <= GEMM_TOL
+
+
+def test_gemm_pair_kernel_matches_single_cta_kernel():
+    """The cta_group::2 kernel and the 1-CTA kernel (MOSS_GEMM_VARIANT=1 in a
+    subprocess) agree to FP32-accumulation noise on the same operands."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, torch, numpy as np
+sys.path.insert(0, ".")
+from paper_2511_05811_b200.quantize import quantize_mx2, quant_per_tensor
+from paper_2511_05811_b200.gemm import mx_gemm
+torch.manual_seed(5)
+a = torch.randn(1024, 2048, device="cuda"); b = torch.randn(768, 2048, device="cuda")
+qa = quantize_mx2(a); qb = quant_per_tensor(b)
+for dt in (torch.float32, torch.bfloat16):
+    d = mx_gemm(qa.codes, qa.sf, qa.g, qb.codes, None, qb.scale.reshape(1), out_dtype=dt)
+    np.save(sys.argv[1] + ("_f32.npy" if dt == torch.float32 else "_bf16.npy"), d.float().cpu().numpy())
+'''
+    import os
+    import tempfile
+    outs = {}
+    for v in ("1", "2"):
+        p = os.path.join(tempfile.mkdtemp(), "g")
+        env = dict(os.environ, MOSS_GEMM_VARIANT=v)
+        subprocess.run([sys.executable, "-c", code, p], check=True, env=env, cwd=os.path.dirname(os.path.dirname(__file__)))
+        outs[v] = (np.load(p + "_f32.npy"), np.load(p + "_bf16.npy"))
+    assert rel_frob(outs["2"][0], outs["1"][0]) <= 1e-6
+    assert rel_frob(outs["2"][1], outs["1"][1]) <= 4e-3
 
 
 # ----------------------------------------------------------------- AdamW
