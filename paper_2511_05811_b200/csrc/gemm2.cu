@@ -7,22 +7,26 @@
 //
 // A cluster of two CTAs on one TPC computes a 256 x 256 tile with
 // tcgen05.mma.cta_group::2 (M = 256): each CTA stages its own 128 rows of A
-// and half (128 rows) of B, so a pair moves 2 x 32 KB of operands per 128-K
-// stage instead of the 2 x 48 KB two independent 128 x 256 CTAs would — the
-// L2 -> SM traffic that bounds the 1-CTA kernel drops by a third.
+// and one half (128 rows) of B, so a pair moves 2 x 32 KB of operands per
+// 128-K stage where two independent 128 x 256 CTAs move 2 x 48 KB.  The
+// 1-CTA kernel is latency-bound on its 4 x 48 KB ring; the pair kernel keeps
+// more stages in flight (32 KB + SF per stage) for the same FLOPs.
+//
+// Every load — A, B and both scale-factor operands — is a 2-SM TMA whose
+// bytes are credited to the LEADER CTA's full barrier, so the MMA issuer
+// waits on exactly one barrier per stage.
 //
 // Roles (per CTA, 640 threads):
-//   warp 0       TMA producer: 2-SM TMA loads of A/B (bytes credited to the
-//                leader's full barrier), bulk copies of this CTA's SF
-//   warp 1       leader only: MMA issuer (tcgen05.cp + tcgen05.mma cta_group::2,
-//                multicast commits to both CTAs' empty / tmem_full barriers)
+//   warp 0       TMA producer (both CTAs)
+//   warp 1       MMA issuer (leader CTA, one thread): tcgen05.cp + tcgen05.mma
+//                cta_group::2, multicast commits to both CTAs' barriers
 //   warp 2       TMEM allocator (cta_group::2)
-//   warp 3       SF watcher: waits this CTA's SF bytes, then arrives on the
-//                leader's full barrier (so the leader knows both SF halves landed)
 //   warps 4-19   epilogue: 4 warps per TMEM lane quadrant, 64 columns each;
-//                tcgen05.ld -> release TMEM to the leader -> alpha -> bf16/f32
-//                -> 128B-swizzled smem -> TMA store (TMA reduce-add for accumulate)
+//                tcgen05.ld -> release TMEM (arrive on the leader) -> alpha ->
+//                bf16/f32 -> global (direct stores, or swizzled smem + TMA store /
+//                TMA reduce-add when TMA_EPI)
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "host_utils.cuh"
@@ -32,35 +36,40 @@ namespace moss {
 constexpr int G2_BM = 128;       // rows per CTA (256 per pair)
 constexpr int G2_BN = 256;       // columns per pair tile
 constexpr int G2_BK = 128;
-constexpr int G2_STAGES = 4;
 constexpr int G2_EPI_WARPS = 16;
 constexpr int G2_THREADS = (4 + G2_EPI_WARPS) * 32;
 
+template <int STAGES, bool TMA_EPI>
 struct G2Layout {
     static constexpr int A_BYTES = G2_BM * G2_BK;              // 16 KB
     static constexpr int B_BYTES = (G2_BN / 2) * G2_BK;        // 16 KB (half of B per CTA)
     static constexpr int SFA_BYTES = 512;
-    static constexpr int SFB_BYTES = (G2_BN / 128) * 512;      // full-N scales in each CTA
+    static constexpr int SFB_BYTES = (G2_BN / 128) * 512;      // scales of all 256 B rows in each CTA
     static constexpr int OFF_A = 0;
-    static constexpr int OFF_B = OFF_A + G2_STAGES * A_BYTES;
-    static constexpr int OFF_SFA = OFF_B + G2_STAGES * B_BYTES;
-    static constexpr int OFF_SFB = OFF_SFA + G2_STAGES * SFA_BYTES;
-    static constexpr int OFF_UNIT = OFF_SFB + G2_STAGES * SFB_BYTES;
-    static constexpr int OFF_STG = OFF_UNIT + SFB_BYTES;       // 16 x 4 KB epilogue staging
-    static constexpr int OFF_BAR = OFF_STG + G2_EPI_WARPS * 4096;
-    static constexpr int N_BARS = 3 * G2_STAGES + 2;          // full, sf_full, empty, tmem_full, tmem_empty
+    static constexpr int OFF_B = OFF_A + STAGES * A_BYTES;
+    static constexpr int OFF_SFA = OFF_B + STAGES * B_BYTES;
+    static constexpr int OFF_SFB = OFF_SFA + STAGES * SFA_BYTES;
+    static constexpr int OFF_UNIT = OFF_SFB + STAGES * SFB_BYTES;
+    static constexpr int STG_BYTES = TMA_EPI ? 2048 : 0;       // per epilogue warp: 32 rows x 64 B
+    static constexpr int OFF_STG = OFF_UNIT + SFB_BYTES;
+    static constexpr int OFF_BAR = OFF_STG + G2_EPI_WARPS * STG_BYTES;
+    static constexpr int N_BARS = 2 * STAGES + 2;             // full, empty, tmem_full, tmem_empty
     static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
     static constexpr int SMEM = OFF_TMEM + 16 + 1024;
-    static constexpr uint32_t TMEM_COLS = 512;                 // 256 accumulator + SF
+    static constexpr uint32_t TMEM_COLS = 512;                 // 256 accumulator + SF columns
 };
 
-template <bool OUT_BF16>
+// SF buffers are viewed as [bytes/256, 256] u8 tensors: one 512 B chunk = box {256, 2}
+__device__ __forceinline__ int sf_row_of_chunk(int64_t chunk) { return (int)(chunk * 2); }
+
+template <bool OUT_BF16, int STAGES, bool TMA_EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
     gemm_mxf8_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                          const __grid_constant__ CUtensorMap tmD, const uint8_t* __restrict__ sfa,
-                          const uint8_t* __restrict__ sfb, const float* __restrict__ sA,
-                          const float* __restrict__ sB, int M, int N, int K, int accumulate) {
-    using L = G2Layout;
+                          const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
+                          const __grid_constant__ CUtensorMap tmD, void* __restrict__ D, int64_t ldd,
+                          const float* __restrict__ sA, const float* __restrict__ sB, int M, int N, int K,
+                          int unit_b, int accumulate) {
+    using L = G2Layout<STAGES, TMA_EPI>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* s_a = smem + L::OFF_A;
@@ -69,11 +78,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
     uint8_t* s_sfb = smem + L::OFF_SFB;
     uint8_t* s_unit = smem + L::OFF_UNIT;
     uint8_t* s_stg = smem + L::OFF_STG;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);   // leader's is the live one
-    uint64_t* sf_full = full + G2_STAGES;
-    uint64_t* empty = sf_full + G2_STAGES;
-    uint64_t* tmem_full = empty + G2_STAGES;
-    uint64_t* tmem_empty = tmem_full + 1;                              // leader's is the live one
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);   // the leader's are live
+    uint64_t* empty = full + STAGES;
+    uint64_t* tmem_full = empty + STAGES;
+    uint64_t* tmem_empty = tmem_full + 1;                              // the leader's is live
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -82,17 +90,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     const int m_pairs = M / (2 * G2_BM), n_tiles = N / G2_BN, num_tiles = m_pairs * n_tiles;
     const int kblocks = K / G2_BK;
-    const bool unit_b = (sfb == nullptr);
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmA);
         prefetch_tmap(&tmB);
-        prefetch_tmap(&tmD);
+        prefetch_tmap(&tmSFA);
+        if (!unit_b) prefetch_tmap(&tmSFB);
+        if (TMA_EPI) prefetch_tmap(&tmD);
     }
     if (warp == 1 && lane == 0) {
-        for (int s = 0; s < G2_STAGES; ++s) {
-            mbar_init(&full[s], 2);        // one SF-watcher arrival per CTA (+ A/B tx bytes of both)
-            mbar_init(&sf_full[s], 1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);        // leader's arrive.expect_tx; bytes from both CTAs
             mbar_init(&empty[s], 1);
         }
         mbar_init(tmem_full, 1);
@@ -110,53 +118,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
     const uint32_t tmem = *tmem_slot;
     const uint32_t tm_sfa = tmem + G2_BN;
     const uint32_t tm_sfb = tmem + G2_BN + 4;
-    const uint32_t full_leader0 = mapa_shared(&full[0], 0);
-    const uint32_t tmem_empty_leader = mapa_shared(tmem_empty, 0);
 
     if (warp == 0) {
         // ---------------- producer (both CTAs) ----------------
         if (lane == 0) {
+            const uint32_t full_leader0 = mapa_shared(&full[0], 0);
+            const uint32_t cta_bytes = L::A_BYTES + L::B_BYTES + L::SFA_BYTES + (unit_b ? 0 : L::SFB_BYTES);
             int stage = 0;
             uint32_t phase = 0;
-            const uint32_t ab_bytes = L::A_BYTES + L::B_BYTES;
-            const uint32_t sf_bytes = L::SFA_BYTES + (unit_b ? 0 : L::SFB_BYTES);
             for (int tile = pair; tile < num_tiles; tile += npairs) {
                 const int mp = tile % m_pairs, nt = tile / m_pairs;
-                const int mb = mp * 2 + rank;                       // this CTA's 128-row block
+                const int mb = mp * 2 + rank;                       // this CTA's 128-row block of A
                 const int n0 = nt * G2_BN + rank * (G2_BN / 2);     // this CTA's half of B
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if (leader) mbar_expect_tx(&full[stage], 2 * ab_bytes);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * cta_bytes);
                     const uint32_t fl = full_leader0 + stage * 8;
                     tma_load_2d_2sm(s_a + stage * L::A_BYTES, &tmA, fl, kb * G2_BK, mb * G2_BM);
                     tma_load_2d_2sm(s_b + stage * L::B_BYTES, &tmB, fl, kb * G2_BK, n0);
-                    mbar_arrive_expect_tx(&sf_full[stage], sf_bytes);
-                    bulk_load(s_sfa + stage * L::SFA_BYTES, sfa + ((int64_t)mb * kblocks + kb) * 512, 512,
-                              &sf_full[stage]);
+                    tma_load_2d_2sm(s_sfa + stage * L::SFA_BYTES, &tmSFA, fl, 0,
+                                    sf_row_of_chunk((int64_t)mb * kblocks + kb));
                     if (!unit_b) {
 #pragma unroll
                         for (int j = 0; j < G2_BN / 128; ++j)
-                            bulk_load(s_sfb + stage * L::SFB_BYTES + j * 512,
-                                      sfb + ((int64_t)(nt * (G2_BN / 128) + j) * kblocks + kb) * 512, 512,
-                                      &sf_full[stage]);
+                            tma_load_2d_2sm(s_sfb + stage * L::SFB_BYTES + j * 512, &tmSFB, fl, 0,
+                                            sf_row_of_chunk((int64_t)(nt * (G2_BN / 128) + j) * kblocks + kb));
                     }
-                    if (++stage == G2_STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
-            }
-        }
-    } else if (warp == 3) {
-        // ---------------- SF watcher (both CTAs) ----------------
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = pair; tile < num_tiles; tile += npairs) {
-                for (int kb = 0; kb < kblocks; ++kb) {
-                    mbar_wait(&sf_full[stage], phase);
-                    mbar_arrive_cluster(full_leader0 + stage * 8);
-                    if (++stage == G2_STAGES) {
+                    if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -191,10 +179,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
                     const uint64_t bdesc = umma_desc(smem_u32(s_b + stage * L::B_BYTES), 0, 1024, kLayoutSW128);
 #pragma unroll
                     for (int k = 0; k < G2_BK / 32; ++k)
-                        mma_mxf8_2cta(tmem, adesc + 2 * k, bdesc + 2 * k, idesc0 | ((uint32_t)k << 29) | ((uint32_t)k << 4),
-                                      tm_sfa, tm_sfb, (kb | k) != 0);
+                        mma_mxf8_2cta(tmem, adesc + 2 * k, bdesc + 2 * k,
+                                      idesc0 | ((uint32_t)k << 29) | ((uint32_t)k << 4), tm_sfa, tm_sfb, (kb | k) != 0);
                     tc_commit_2cta_mc(&empty[stage], 0x3);
-                    if (++stage == G2_STAGES) {
+                    if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -207,8 +195,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
         // ---------------- epilogue (both CTAs) ----------------
         const int ew = warp - 4;
         const int quad = warp & 3;            // TMEM lanes [32*quad, 32*quad+32)
-        const int cq = ew >> 2;               // 64-column quarter
-        uint8_t* stg = s_stg + ew * 4096;     // 32 rows x 128 B, SWIZZLE_128B
+        const int cq = ew >> 2;               // 64-column quarter of the 256-column tile
+        const uint32_t tmem_empty_leader = mapa_shared(tmem_empty, 0);
+        uint8_t* stg = s_stg + ew * L::STG_BYTES;
         const float alpha = __fmul_rn(*sA, *sB);
         uint32_t acc_phase = 0;
         for (int tile = pair; tile < num_tiles; tile += npairs) {
@@ -226,50 +215,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tmem_empty_leader);   // accumulator may be overwritten now
             acc_phase ^= 1;
-            if (OUT_BF16) {
-                if (lane == 0) bulk_wait_read0();
-                __syncwarp();
+            if (!TMA_EPI) {
+                const int64_t row = row0 + lane;
+                if (OUT_BF16) {
+                    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(D) + row * ldd + col0);
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    uint4 o;
-                    o.x = pack_bf16(__uint_as_float(r[8 * c + 0]) * alpha, __uint_as_float(r[8 * c + 1]) * alpha);
-                    o.y = pack_bf16(__uint_as_float(r[8 * c + 2]) * alpha, __uint_as_float(r[8 * c + 3]) * alpha);
-                    o.z = pack_bf16(__uint_as_float(r[8 * c + 4]) * alpha, __uint_as_float(r[8 * c + 5]) * alpha);
-                    o.w = pack_bf16(__uint_as_float(r[8 * c + 6]) * alpha, __uint_as_float(r[8 * c + 7]) * alpha);
-                    *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) = o;
-                }
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    tma_store_2d(&tmD, stg, col0, row0);
-                    bulk_commit();
+                    for (int c = 0; c < 8; ++c) {
+                        uint4 o;
+                        o.x = pack_bf16(__uint_as_float(r[8 * c + 0]) * alpha, __uint_as_float(r[8 * c + 1]) * alpha);
+                        o.y = pack_bf16(__uint_as_float(r[8 * c + 2]) * alpha, __uint_as_float(r[8 * c + 3]) * alpha);
+                        o.z = pack_bf16(__uint_as_float(r[8 * c + 4]) * alpha, __uint_as_float(r[8 * c + 5]) * alpha);
+                        o.w = pack_bf16(__uint_as_float(r[8 * c + 6]) * alpha, __uint_as_float(r[8 * c + 7]) * alpha);
+                        dst[c] = o;
+                    }
+                } else {
+                    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(D) + row * ldd + col0);
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        float4 o = make_float4(__uint_as_float(r[4 * c + 0]) * alpha, __uint_as_float(r[4 * c + 1]) * alpha,
+                                               __uint_as_float(r[4 * c + 2]) * alpha, __uint_as_float(r[4 * c + 3]) * alpha);
+                        if (accumulate) {
+                            const float4 p = dst[c];
+                            o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+                        }
+                        dst[c] = o;
+                    }
                 }
             } else {
+                // 32 rows x 64 B chunks, SWIZZLE_64B (16 B chunk ^ (row >> 1) & 3); 2 (bf16) or 4 (f32) chunks
+                constexpr int NCH = OUT_BF16 ? 2 : 4;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < NCH; ++h) {
                     if (lane == 0) bulk_wait_read0();
                     __syncwarp();
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const float4 o = make_float4(__uint_as_float(r[32 * h + 4 * c + 0]) * alpha,
-                                                     __uint_as_float(r[32 * h + 4 * c + 1]) * alpha,
-                                                     __uint_as_float(r[32 * h + 4 * c + 2]) * alpha,
-                                                     __uint_as_float(r[32 * h + 4 * c + 3]) * alpha);
-                        *reinterpret_cast<float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) = o;
+                    for (int c = 0; c < 4; ++c) {
+                        uint4 o;
+                        if (OUT_BF16) {
+                            const uint32_t* q = &r[32 * h + 8 * c];
+                            o.x = pack_bf16(__uint_as_float(q[0]) * alpha, __uint_as_float(q[1]) * alpha);
+                            o.y = pack_bf16(__uint_as_float(q[2]) * alpha, __uint_as_float(q[3]) * alpha);
+                            o.z = pack_bf16(__uint_as_float(q[4]) * alpha, __uint_as_float(q[5]) * alpha);
+                            o.w = pack_bf16(__uint_as_float(q[6]) * alpha, __uint_as_float(q[7]) * alpha);
+                        } else {
+                            const uint32_t* q = &r[16 * h + 4 * c];
+                            o.x = __float_as_uint(__uint_as_float(q[0]) * alpha);
+                            o.y = __float_as_uint(__uint_as_float(q[1]) * alpha);
+                            o.z = __float_as_uint(__uint_as_float(q[2]) * alpha);
+                            o.w = __float_as_uint(__uint_as_float(q[3]) * alpha);
+                        }
+                        *reinterpret_cast<uint4*>(stg + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) = o;
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        if (accumulate)
-                            tma_reduce_add_2d(&tmD, stg, col0 + 32 * h, row0);
+                        const int c0 = col0 + h * (OUT_BF16 ? 32 : 16);
+                        if (!OUT_BF16 && accumulate)
+                            tma_reduce_add_2d(&tmD, stg, c0, row0);
                         else
-                            tma_store_2d(&tmD, stg, col0 + 32 * h, row0);
+                            tma_store_2d(&tmD, stg, c0, row0);
                         bulk_commit();
                     }
                 }
             }
         }
-        if (lane == 0) bulk_wait0();
+        if (TMA_EPI && lane == 0) bulk_wait0();
     }
     tc_fence_before();
     cluster_sync_all();
@@ -279,40 +289,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
     }
 }
 
-template <bool OUT_BF16>
+template <bool OUT_BF16, int STAGES, bool TMA_EPI>
 static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
                           const float* sB, void* D, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
                           cudaStream_t st) {
-    using L = G2Layout;
-    auto kern = gemm_mxf8_2cta_kernel<OUT_BF16>;
+    using L = G2Layout<STAGES, TMA_EPI>;
+    auto kern = gemm_mxf8_2cta_kernel<OUT_BF16, STAGES, TMA_EPI>;
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM) != cudaSuccess)
             return MOSS_ERR_CUDA;
         attr_set = true;
     }
-    CUtensorMap ta, tb, td;
+    CUtensorMap ta, tb, tsa, tsb, td;
+    const int64_t sfa_rows = ((M + 127) / 128) * (K / 128) * 2;
+    const int64_t sfb_rows = ((N + 127) / 128) * (K / 128) * 2;
     if (!make_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, A, M, K, 128, G2_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, B, N, K, 128, G2_BN / 2, CU_TENSOR_MAP_SWIZZLE_128B))
+        !make_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, B, N, K, 128, G2_BN / 2, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap_2d(&tsa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, SFA, sfa_rows, 256, 256, 2, CU_TENSOR_MAP_SWIZZLE_NONE))
         return MOSS_ERR_CUDA;
-    // D: [M, ldd] row-major; 32-row x 128 B boxes (64 bf16 or 32 f32 columns)
-    {
+    tsb = tsa;
+    if (SFB && !make_tmap_2d(&tsb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, SFB, sfb_rows, 256, 256, 2,
+                             CU_TENSOR_MAP_SWIZZLE_NONE))
+        return MOSS_ERR_CUDA;
+    td = ta;
+    if (TMA_EPI) {
         EncodeTiledFn enc = get_encode_fn();
         if (!enc) return MOSS_ERR_CUDA;
         const size_t esz = OUT_BF16 ? 2 : 4;
         cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
         cuuint64_t strides[1] = {(cuuint64_t)(ldd * esz)};
-        cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 32u};
+        cuuint32_t box[2] = {(cuuint32_t)(64 / esz), 32u};
         cuuint32_t estr[2] = {1u, 1u};
         if (enc(&td, OUT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, D, dims, strides,
-                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return MOSS_ERR_CUDA;
     }
     const int64_t tiles = (M / (2 * G2_BM)) * (N / G2_BN);
     const int pairs = (int)std::min<int64_t>(tiles, sm_count() / 2);
-    kern<<<2 * pairs, G2_THREADS, L::SMEM, st>>>(ta, tb, td, SFA, SFB, sA, sB, (int)M, (int)N, (int)K, accumulate);
+    kern<<<2 * pairs, G2_THREADS, L::SMEM, st>>>(ta, tb, tsa, tsb, td, D, ldd, sA, sB, (int)M, (int)N, (int)K,
+                                                 SFB == nullptr, accumulate);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+}
+
+// MOSS_GEMM2_MODE: 0 (default) = 6 stages + direct-store epilogue, 1 = 5 stages + TMA-store epilogue
+static int gemm2_mode() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MOSS_GEMM2_MODE");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v;
 }
 
 // returns -1 when the shape is not covered by the pair kernel
@@ -321,8 +349,11 @@ int launch_gemm2(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const u
                  cudaStream_t st) {
     if (M % (2 * G2_BM) || N % G2_BN || K % G2_BK) return -1;
     if ((reinterpret_cast<uintptr_t>(D) % 16) || (ldd * (d_dtype == MOSS_BF16 ? 2 : 4)) % 16) return -1;
-    return d_dtype == MOSS_BF16 ? launch_gemm2_t<true>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
-                                : launch_gemm2_t<false>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
+    if (gemm2_mode() == 1)
+        return d_dtype == MOSS_BF16 ? launch_gemm2_t<true, 5, true>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
+                                    : launch_gemm2_t<false, 5, true>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
+    return d_dtype == MOSS_BF16 ? launch_gemm2_t<true, 6, false>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
+                                : launch_gemm2_t<false, 6, false>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
 }
 
 }  // namespace moss
