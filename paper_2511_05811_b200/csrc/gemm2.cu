@@ -36,10 +36,8 @@ namespace moss {
 constexpr int G2_BM = 128;       // rows per CTA (256 per pair)
 constexpr int G2_BN = 256;       // columns per pair tile
 constexpr int G2_BK = 128;
-constexpr int G2_EPI_WARPS = 16;
-constexpr int G2_THREADS = (4 + G2_EPI_WARPS) * 32;
 
-template <int STAGES, bool TMA_EPI>
+template <int STAGES, bool TMA_EPI, int EPI_WARPS>
 struct G2Layout {
     static constexpr int A_BYTES = G2_BM * G2_BK;              // 16 KB
     static constexpr int B_BYTES = (G2_BN / 2) * G2_BK;        // 16 KB (half of B per CTA)
@@ -52,7 +50,7 @@ struct G2Layout {
     static constexpr int OFF_UNIT = OFF_SFB + STAGES * SFB_BYTES;
     static constexpr int STG_BYTES = TMA_EPI ? 2048 : 0;       // per epilogue warp: 32 rows x 64 B
     static constexpr int OFF_STG = OFF_UNIT + SFB_BYTES;
-    static constexpr int OFF_BAR = OFF_STG + G2_EPI_WARPS * STG_BYTES;
+    static constexpr int OFF_BAR = OFF_STG + EPI_WARPS * STG_BYTES;
     static constexpr int N_BARS = 2 * STAGES + 2;             // full, empty, tmem_full, tmem_empty
     static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
     static constexpr int SMEM = OFF_TMEM + 16 + 1024;
@@ -62,14 +60,15 @@ struct G2Layout {
 // SF buffers are viewed as [bytes/256, 256] u8 tensors: one 512 B chunk = box {256, 2}
 __device__ __forceinline__ int sf_row_of_chunk(int64_t chunk) { return (int)(chunk * 2); }
 
-template <bool OUT_BF16, int STAGES, bool TMA_EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
+template <bool OUT_BF16, int STAGES, bool TMA_EPI, int EPI_WARPS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32, 1)
     gemm_mxf8_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
                           const __grid_constant__ CUtensorMap tmD, void* __restrict__ D, int64_t ldd,
                           const float* __restrict__ sA, const float* __restrict__ sB, int M, int N, int K,
                           int unit_b, int accumulate) {
-    using L = G2Layout<STAGES, TMA_EPI>;
+    using L = G2Layout<STAGES, TMA_EPI, EPI_WARPS>;
+    constexpr int COLS = G2_BN / (EPI_WARPS / 4);   // accumulator columns per epilogue warp
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* s_a = smem + L::OFF_A;
@@ -104,7 +103,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
             mbar_init(&empty[s], 1);
         }
         mbar_init(tmem_full, 1);
-        mbar_init(tmem_empty, 2 * G2_EPI_WARPS);
+        mbar_init(tmem_empty, 2 * EPI_WARPS);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc_2cta(tmem_slot, L::TMEM_COLS);
@@ -195,7 +194,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
         // ---------------- epilogue (both CTAs) ----------------
         const int ew = warp - 4;
         const int quad = warp & 3;            // TMEM lanes [32*quad, 32*quad+32)
-        const int cq = ew >> 2;               // 64-column quarter of the 256-column tile
+        const int cq = ew >> 2;               // column slice of the 256-column tile
         const uint32_t tmem_empty_leader = mapa_shared(tmem_empty, 0);
         uint8_t* stg = s_stg + ew * L::STG_BYTES;
         const float alpha = __fmul_rn(*sA, *sB);
@@ -203,13 +202,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
         for (int tile = pair; tile < num_tiles; tile += npairs) {
             const int mp = tile % m_pairs, nt = tile / m_pairs;
             const int row0 = (mp * 2 + rank) * G2_BM + quad * 32;
-            const int col0 = nt * G2_BN + cq * 64;
+            const int col0 = nt * G2_BN + cq * COLS;
             mbar_wait(tmem_full, acc_phase);
             tc_fence_after();
-            uint32_t r[64];
-            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + cq * 64;
-            tmem_ld32(ta, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-            tmem_ld32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+            uint32_t r[COLS];
+            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + cq * COLS;
+#pragma unroll
+            for (int c = 0; c < COLS / 32; ++c) tmem_ld32(ta + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&r[32 * c]));
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
@@ -220,7 +219,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
                 if (OUT_BF16) {
                     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(D) + row * ldd + col0);
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
+                    for (int c = 0; c < COLS / 8; ++c) {
                         uint4 o;
                         o.x = pack_bf16(__uint_as_float(r[8 * c + 0]) * alpha, __uint_as_float(r[8 * c + 1]) * alpha);
                         o.y = pack_bf16(__uint_as_float(r[8 * c + 2]) * alpha, __uint_as_float(r[8 * c + 3]) * alpha);
@@ -231,7 +230,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
                 } else {
                     float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(D) + row * ldd + col0);
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) {
+                    for (int c = 0; c < COLS / 4; ++c) {
                         float4 o = make_float4(__uint_as_float(r[4 * c + 0]) * alpha, __uint_as_float(r[4 * c + 1]) * alpha,
                                                __uint_as_float(r[4 * c + 2]) * alpha, __uint_as_float(r[4 * c + 3]) * alpha);
                         if (accumulate) {
@@ -242,8 +241,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
                     }
                 }
             } else {
-                // 32 rows x 64 B chunks, SWIZZLE_64B (16 B chunk ^ (row >> 1) & 3); 2 (bf16) or 4 (f32) chunks
-                constexpr int NCH = OUT_BF16 ? 2 : 4;
+                // 32 rows x 64 B pieces, SWIZZLE_64B (16 B chunk ^ (row >> 1) & 3)
+                constexpr int EPC = OUT_BF16 ? 32 : 16;          // elements per 64 B piece
+                constexpr int NCH = COLS / EPC;
 #pragma unroll
                 for (int h = 0; h < NCH; ++h) {
                     if (lane == 0) bulk_wait_read0();
@@ -269,7 +269,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        const int c0 = col0 + h * (OUT_BF16 ? 32 : 16);
+                        const int c0 = col0 + h * EPC;
                         if (!OUT_BF16 && accumulate)
                             tma_reduce_add_2d(&tmD, stg, c0, row0);
                         else
@@ -289,12 +289,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
     }
 }
 
-template <bool OUT_BF16, int STAGES, bool TMA_EPI>
+template <bool OUT_BF16, int STAGES, bool TMA_EPI, int EPI_WARPS>
 static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
                           const float* sB, void* D, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
                           cudaStream_t st) {
-    using L = G2Layout<STAGES, TMA_EPI>;
-    auto kern = gemm_mxf8_2cta_kernel<OUT_BF16, STAGES, TMA_EPI>;
+    using L = G2Layout<STAGES, TMA_EPI, EPI_WARPS>;
+    auto kern = gemm_mxf8_2cta_kernel<OUT_BF16, STAGES, TMA_EPI, EPI_WARPS>;
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM) != cudaSuccess)
@@ -328,18 +328,21 @@ static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B
     }
     const int64_t tiles = (M / (2 * G2_BM)) * (N / G2_BN);
     const int pairs = (int)std::min<int64_t>(tiles, sm_count() / 2);
-    kern<<<2 * pairs, G2_THREADS, L::SMEM, st>>>(ta, tb, tsa, tsb, td, D, ldd, sA, sB, (int)M, (int)N, (int)K,
+    kern<<<2 * pairs, (4 + EPI_WARPS) * 32, L::SMEM, st>>>(ta, tb, tsa, tsb, td, D, ldd, sA, sB, (int)M, (int)N, (int)K,
                                                  SFB == nullptr, accumulate);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 
-// MOSS_GEMM2_MODE: 1 (default) = 5 stages + TMA-store epilogue, 0 = 6 stages + direct-store epilogue
-// (measured on B200, config-2 shapes: mode 1 is 2-4 % faster)
+// MOSS_GEMM2_MODE (A/B testing on B200):
+//   2 (default) 6 stages, 8 epilogue warps x 128 columns, TMA-store epilogue
+//   1           5 stages, 16 epilogue warps x 64 columns, TMA-store epilogue
+//   0           6 stages, 16 epilogue warps, direct-store epilogue
 static int gemm2_mode() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("MOSS_GEMM2_MODE");
-        v = (e && e[0] == '0') ? 0 : 1;
+        v = e ? (e[0] - '0') : 2;
+        if (v < 0 || v > 2) v = 2;
     }
     return v;
 }
@@ -350,11 +353,18 @@ int launch_gemm2(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const u
                  cudaStream_t st) {
     if (M % (2 * G2_BM) || N % G2_BN || K % G2_BK) return -1;
     if ((reinterpret_cast<uintptr_t>(D) % 16) || (ldd * (d_dtype == MOSS_BF16 ? 2 : 4)) % 16) return -1;
-    if (gemm2_mode() == 1)
-        return d_dtype == MOSS_BF16 ? launch_gemm2_t<true, 5, true>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
-                                    : launch_gemm2_t<false, 5, true>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
-    return d_dtype == MOSS_BF16 ? launch_gemm2_t<true, 6, false>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
-                                : launch_gemm2_t<false, 6, false>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
+    const bool bf = d_dtype == MOSS_BF16;
+    switch (gemm2_mode()) {
+        case 1:
+            return bf ? launch_gemm2_t<true, 5, true, 16>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
+                      : launch_gemm2_t<false, 5, true, 16>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
+        case 0:
+            return bf ? launch_gemm2_t<true, 6, false, 16>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
+                      : launch_gemm2_t<false, 6, false, 16>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
+        default:
+            return bf ? launch_gemm2_t<true, 6, true, 8>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
+                      : launch_gemm2_t<false, 6, true, 8>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
+    }
 }
 
 }  // namespace moss
