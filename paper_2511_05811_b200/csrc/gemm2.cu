@@ -115,8 +115,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // SF columns double-buffered by k-block parity: [256, 268) and [272, 284)
     const uint32_t tm_sfa = tmem + G2_BN;
     const uint32_t tm_sfb = tmem + G2_BN + 4;
+    constexpr uint32_t SF_ALT = 16;
 
     if (warp == 0) {
         // ---------------- producer (both CTAs) ----------------
@@ -155,11 +157,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
         if (leader && lane == 0) {
             if (unit_b) {
 #pragma unroll
-                for (int j = 0; j < G2_BN / 128; ++j)
+                for (int j = 0; j < G2_BN / 128; ++j) {
                     tmem_cp_sf_2cta(tm_sfb + j * 4, umma_desc(smem_u32(s_unit + j * 512), 0, 128, kLayoutNone));
+                    tmem_cp_sf_2cta(tm_sfb + SF_ALT + j * 4, umma_desc(smem_u32(s_unit + j * 512), 0, 128, kLayoutNone));
+                }
             }
             int stage = 0;
-            uint32_t phase = 0, acc_phase = 0;
+            uint32_t phase = 0, acc_phase = 0, sfbuf = 0;
             constexpr uint32_t idesc0 = mxf8_idesc(2 * G2_BM, G2_BN, 0, 0);
             for (int tile = pair; tile < num_tiles; tile += npairs) {
                 mbar_wait(tmem_empty, acc_phase ^ 1);
@@ -167,20 +171,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    tmem_cp_sf_2cta(tm_sfa, umma_desc(smem_u32(s_sfa + stage * L::SFA_BYTES), 0, 128, kLayoutNone));
+                    const uint32_t sa = tm_sfa + sfbuf, sb = tm_sfb + sfbuf;
+                    tmem_cp_sf_2cta(sa, umma_desc(smem_u32(s_sfa + stage * L::SFA_BYTES), 0, 128, kLayoutNone));
                     if (!unit_b) {
 #pragma unroll
                         for (int j = 0; j < G2_BN / 128; ++j)
-                            tmem_cp_sf_2cta(tm_sfb + j * 4, umma_desc(smem_u32(s_sfb + stage * L::SFB_BYTES + j * 512),
-                                                                      0, 128, kLayoutNone));
+                            tmem_cp_sf_2cta(sb + j * 4, umma_desc(smem_u32(s_sfb + stage * L::SFB_BYTES + j * 512),
+                                                                  0, 128, kLayoutNone));
                     }
                     const uint64_t adesc = umma_desc(smem_u32(s_a + stage * L::A_BYTES), 0, 1024, kLayoutSW128);
                     const uint64_t bdesc = umma_desc(smem_u32(s_b + stage * L::B_BYTES), 0, 1024, kLayoutSW128);
 #pragma unroll
                     for (int k = 0; k < G2_BK / 32; ++k)
                         mma_mxf8_2cta(tmem, adesc + 2 * k, bdesc + 2 * k,
-                                      idesc0 | ((uint32_t)k << 29) | ((uint32_t)k << 4), tm_sfa, tm_sfb, (kb | k) != 0);
+                                      idesc0 | ((uint32_t)k << 29) | ((uint32_t)k << 4), sa, sb, (kb | k) != 0);
                     tc_commit_2cta_mc(&empty[stage], 0x3);
+                    sfbuf ^= SF_ALT;
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
