@@ -99,15 +99,15 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     const uint32_t tm_sfb = tmem + BN + 4;
 
     if (warp == 0) {
-        // ---------------- TMA producer ----------------
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            const uint32_t bytes = L::A_BYTES + L::B_BYTES + 512 + (unit_b ? 0 : L::SFB_BYTES);
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const int mb = tile % m_tiles, nb = tile / m_tiles;
-                for (int kb = 0; kb < kblocks; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
+        // ---------------- TMA producer (warp-converged, one elected lane issues) ----------------
+        int stage = 0;
+        uint32_t phase = 0;
+        const uint32_t bytes = L::A_BYTES + L::B_BYTES + 512 + (unit_b ? 0 : L::SFB_BYTES);
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const int mb = tile % m_tiles, nb = tile / m_tiles;
+            for (int kb = 0; kb < kblocks; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                if (elect_one()) {
                     mbar_arrive_expect_tx(&full[stage], bytes);
                     tma_load_2d(s_a + stage * L::A_BYTES, &tmA, &full[stage], kb * G_BK, mb * G_BM);
                     tma_load_2d(s_b + stage * L::B_BYTES, &tmB, &full[stage], kb * G_BK, nb * BN);
@@ -118,52 +118,60 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                             bulk_load(s_sfb + stage * L::SFB_BYTES + j * 512,
                                       sfb + ((int64_t)(nb * (BN / 128) + j) * kblocks + kb) * 512, 512, &full[stage]);
                     }
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                }
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer (single thread) ----------------
-        if (lane == 0) {
-            if (unit_b) {
+        // ---------------- MMA issuer (warp-converged, one elected lane issues) ----------------
+        if (unit_b) {
+            if (elect_one()) {
 #pragma unroll
                 for (int j = 0; j < BN / 128; ++j)
                     tmem_cp_sf(tm_sfb + j * 4, umma_desc(smem_u32(s_unit + j * 512), 0, 128, kLayoutNone));
             }
-            int stage = 0;
-            uint32_t phase = 0, acc_phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                mbar_wait(tmem_empty, acc_phase ^ 1);
+            __syncwarp();
+        }
+        int stage = 0;
+        uint32_t phase = 0, acc_phase = 0;
+        const uint64_t adesc0 = umma_desc(smem_u32(s_a), 0, 1024, kLayoutSW128);
+        const uint64_t bdesc0 = umma_desc(smem_u32(s_b), 0, 1024, kLayoutSW128);
+        const uint64_t sfadesc0 = umma_desc(smem_u32(s_sfa), 0, 128, kLayoutNone);
+        const uint64_t sfbdesc0 = umma_desc(smem_u32(s_sfb), 0, 128, kLayoutNone);
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            mbar_wait(tmem_empty, acc_phase ^ 1);
+            tc_fence_after();
+            for (int kb = 0; kb < kblocks; ++kb) {
+                mbar_wait(&full[stage], phase);
                 tc_fence_after();
-                for (int kb = 0; kb < kblocks; ++kb) {
-                    mbar_wait(&full[stage], phase);
-                    tc_fence_after();
-                    tmem_cp_sf(tm_sfa, umma_desc(smem_u32(s_sfa + stage * 512), 0, 128, kLayoutNone));
+                if (elect_one()) {
+                    tmem_cp_sf(tm_sfa, sfadesc0 + (uint64_t)((stage * 512) >> 4));
                     if (!unit_b) {
 #pragma unroll
                         for (int j = 0; j < BN / 128; ++j)
-                            tmem_cp_sf(tm_sfb + j * 4, umma_desc(smem_u32(s_sfb + stage * L::SFB_BYTES + j * 512), 0,
-                                                                 128, kLayoutNone));
+                            tmem_cp_sf(tm_sfb + j * 4, sfbdesc0 + (uint64_t)((stage * L::SFB_BYTES + j * 512) >> 4));
                     }
-                    const uint64_t adesc = umma_desc(smem_u32(s_a + stage * L::A_BYTES), 0, 1024, kLayoutSW128);
-                    const uint64_t bdesc = umma_desc(smem_u32(s_b + stage * L::B_BYTES), 0, 1024, kLayoutSW128);
+                    const uint64_t adesc = adesc0 + (uint64_t)((stage * L::A_BYTES) >> 4);
+                    const uint64_t bdesc = bdesc0 + (uint64_t)((stage * L::B_BYTES) >> 4);
 #pragma unroll
-                    for (int k = 0; k < G_BK / 32; ++k) {
+                    for (int k = 0; k < G_BK / 32; ++k)
                         mma_mxf8(tm_acc, adesc + 2 * k, bdesc + 2 * k, mxf8_idesc(G_BM, BN, k, k), tm_sfa, tm_sfb,
                                  (kb | k) != 0);
-                    }
                     tc_commit(&empty[stage]);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
                 }
-                tc_commit(tmem_full);
-                acc_phase ^= 1;
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
             }
+            if (elect_one()) tc_commit(tmem_full);
+            __syncwarp();
+            acc_phase ^= 1;
         }
     } else if (warp >= 4) {
         // ---------------- epilogue ----------------

@@ -121,18 +121,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
     constexpr uint32_t SF_ALT = 16;
 
     if (warp == 0) {
-        // ---------------- producer (both CTAs) ----------------
-        if (lane == 0) {
-            const uint32_t full_leader0 = mapa_shared(&full[0], 0);
-            const uint32_t cta_bytes = L::A_BYTES + L::B_BYTES + L::SFA_BYTES + (unit_b ? 0 : L::SFB_BYTES);
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = pair; tile < num_tiles; tile += npairs) {
-                const int mp = tile % m_pairs, nt = tile / m_pairs;
-                const int mb = mp * 2 + rank;                       // this CTA's 128-row block of A
-                const int n0 = nt * G2_BN + rank * (G2_BN / 2);     // this CTA's half of B
-                for (int kb = 0; kb < kblocks; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
+        // ---------------- producer (both CTAs; warp-converged, one elected lane issues) ----------------
+        const uint32_t full_leader0 = mapa_shared(&full[0], 0);
+        const uint32_t cta_bytes = L::A_BYTES + L::B_BYTES + L::SFA_BYTES + (unit_b ? 0 : L::SFB_BYTES);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = pair; tile < num_tiles; tile += npairs) {
+            const int mp = tile % m_pairs, nt = tile / m_pairs;
+            const int mb = mp * 2 + rank;                       // this CTA's 128-row block of A
+            const int n0 = nt * G2_BN + rank * (G2_BN / 2);     // this CTA's half of B
+            for (int kb = 0; kb < kblocks; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                if (elect_one()) {
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * cta_bytes);
                     const uint32_t fl = full_leader0 + stage * 8;
                     tma_load_2d_2sm(s_a + stage * L::A_BYTES, &tmA, fl, kb * G2_BK, mb * G2_BM);
@@ -145,54 +145,66 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                             tma_load_2d_2sm(s_sfb + stage * L::SFB_BYTES + j * 512, &tmSFB, fl, 0,
                                             sf_row_of_chunk((int64_t)(nt * (G2_BN / 128) + j) * kblocks + kb));
                     }
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                }
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer (leader CTA, one thread) ----------------
-        if (leader && lane == 0) {
+        // ---------------- MMA issuer (leader CTA; warp-converged, one elected lane issues) ----------------
+        if (leader) {
             if (unit_b) {
+                if (elect_one()) {
 #pragma unroll
-                for (int j = 0; j < G2_BN / 128; ++j) {
-                    tmem_cp_sf_2cta(tm_sfb + j * 4, umma_desc(smem_u32(s_unit + j * 512), 0, 128, kLayoutNone));
-                    tmem_cp_sf_2cta(tm_sfb + SF_ALT + j * 4, umma_desc(smem_u32(s_unit + j * 512), 0, 128, kLayoutNone));
+                    for (int j = 0; j < G2_BN / 128; ++j) {
+                        tmem_cp_sf_2cta(tm_sfb + j * 4, umma_desc(smem_u32(s_unit + j * 512), 0, 128, kLayoutNone));
+                        tmem_cp_sf_2cta(tm_sfb + SF_ALT + j * 4,
+                                        umma_desc(smem_u32(s_unit + j * 512), 0, 128, kLayoutNone));
+                    }
                 }
+                __syncwarp();
             }
             int stage = 0;
             uint32_t phase = 0, acc_phase = 0, sfbuf = 0;
             constexpr uint32_t idesc0 = mxf8_idesc(2 * G2_BM, G2_BN, 0, 0);
+            const uint64_t adesc0 = umma_desc(smem_u32(s_a), 0, 1024, kLayoutSW128);
+            const uint64_t bdesc0 = umma_desc(smem_u32(s_b), 0, 1024, kLayoutSW128);
+            const uint64_t sfadesc0 = umma_desc(smem_u32(s_sfa), 0, 128, kLayoutNone);
+            const uint64_t sfbdesc0 = umma_desc(smem_u32(s_sfb), 0, 128, kLayoutNone);
             for (int tile = pair; tile < num_tiles; tile += npairs) {
                 mbar_wait(tmem_empty, acc_phase ^ 1);
                 tc_fence_after();
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t sa = tm_sfa + sfbuf, sb = tm_sfb + sfbuf;
-                    tmem_cp_sf_2cta(sa, umma_desc(smem_u32(s_sfa + stage * L::SFA_BYTES), 0, 128, kLayoutNone));
-                    if (!unit_b) {
+                    if (elect_one()) {
+                        const uint32_t sa = tm_sfa + sfbuf, sb = tm_sfb + sfbuf;
+                        tmem_cp_sf_2cta(sa, sfadesc0 + (uint64_t)((stage * L::SFA_BYTES) >> 4));
+                        if (!unit_b) {
 #pragma unroll
-                        for (int j = 0; j < G2_BN / 128; ++j)
-                            tmem_cp_sf_2cta(sb + j * 4, umma_desc(smem_u32(s_sfb + stage * L::SFB_BYTES + j * 512),
-                                                                  0, 128, kLayoutNone));
+                            for (int j = 0; j < G2_BN / 128; ++j)
+                                tmem_cp_sf_2cta(sb + j * 4, sfbdesc0 + (uint64_t)((stage * L::SFB_BYTES + j * 512) >> 4));
+                        }
+                        const uint64_t adesc = adesc0 + (uint64_t)((stage * L::A_BYTES) >> 4);
+                        const uint64_t bdesc = bdesc0 + (uint64_t)((stage * L::B_BYTES) >> 4);
+#pragma unroll
+                        for (int k = 0; k < G2_BK / 32; ++k)
+                            mma_mxf8_2cta(tmem, adesc + 2 * k, bdesc + 2 * k,
+                                          idesc0 | ((uint32_t)k << 29) | ((uint32_t)k << 4), sa, sb, (kb | k) != 0);
+                        tc_commit_2cta_mc(&empty[stage], 0x3);
                     }
-                    const uint64_t adesc = umma_desc(smem_u32(s_a + stage * L::A_BYTES), 0, 1024, kLayoutSW128);
-                    const uint64_t bdesc = umma_desc(smem_u32(s_b + stage * L::B_BYTES), 0, 1024, kLayoutSW128);
-#pragma unroll
-                    for (int k = 0; k < G2_BK / 32; ++k)
-                        mma_mxf8_2cta(tmem, adesc + 2 * k, bdesc + 2 * k,
-                                      idesc0 | ((uint32_t)k << 29) | ((uint32_t)k << 4), sa, sb, (kb | k) != 0);
-                    tc_commit_2cta_mc(&empty[stage], 0x3);
+                    __syncwarp();
                     sfbuf ^= SF_ALT;
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                tc_commit_2cta_mc(tmem_full, 0x3);
+                if (elect_one()) tc_commit_2cta_mc(tmem_full, 0x3);
+                __syncwarp();
                 acc_phase ^= 1;
             }
         }
