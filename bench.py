@@ -323,7 +323,7 @@ def main() -> None:
         "tokens_per_s": world * T / (ms / 1e3),
         "gpu_launches": launches,
         "clocks": clocks.summary(),
-        "roofline": {"bound": "tensor", "kernel": "moss::gemm_mxf8_kernel (tcgen05 mxf8f6f4 block_scale)",
+        "roofline": {"bound": "tensor", "kernel": "moss::gemm_mxf8_2cta_kernel (tcgen05.mma.cta_group::2 kind::mxf8f6f4.block_scale)",
                      "achieved": gemm_tflops, "peak": fp8_peak, "unit": "TFLOP/s", "frac": gemm_tflops / fp8_peak,
                      "peak_source": "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (fp8 dense = 2x bf16)",
                      "frac_of_burst": gemm_tflops / (2.0 * bf16_burst), "traffic": traffic,
