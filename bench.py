@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--tokens", type=int, default=8192)
+    ap.add_argument("--workload", choices=["layer", "llama7b"], default="layer",
+                    help="layer: configs[1] (default); llama7b: configs[3]/[4] Llama-2-7B-shape decoder step")
+    ap.add_argument("--layers", type=int, default=32, help="llama7b: decoder layers (truncate to fit)")
+    ap.add_argument("--seq", type=int, default=4096, help="llama7b: sequence length (batch 1 per GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -191,22 +195,37 @@ def main() -> None:
     from paper_2511_05811_b200.workloads import LayerStack
 
     dev = torch.device("cuda", local)
-    torch.manual_seed(1234 + rank)
-    model = LayerStack(device=dev)
-    opt = MossAdamW(model, lr=3e-4, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1)
+    torch.manual_seed(1234)          # identical initial weights on every rank (DP)
+    if args.workload == "llama7b":
+        from paper_2511_05811_b200.llama import LLAMA2_7B, LlamaConfig, LlamaModel
+        from paper_2511_05811_b200.trainer import make_optimizer
+        cfg = LlamaConfig(**{**LLAMA2_7B.__dict__, "n_layers": args.layers, "max_seq": args.seq})
+        model = LlamaModel(cfg, device=dev)
+        opt = make_optimizer(model, 3e-4, 10_000, 100)
+        T = args.seq
+        g = torch.Generator(device=dev).manual_seed(99 + rank)
+        tok = torch.randint(0, cfg.vocab, (1, T + 1), device=dev, generator=g)
+        x, y_tok = tok[:, :-1].contiguous(), tok[:, 1:].contiguous()
+        flops_step = float(cfg.gemm_flops_per_token()) * T
+        fwd = lambda xin: model(xin, y_tok)
+    else:
+        model = LayerStack(device=dev)
+        opt = MossAdamW(model, lr=3e-4, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1)
+        T = args.tokens
+        torch.manual_seed(4321 + rank)   # per-rank batch shard
+        x = torch.randn(T, model.d, device=dev, dtype=torch.bfloat16)
+        flops_step = float(model.gemm_flops_per_token()) * T
+        fwd = model
     buckets = GradBuckets(model, bucket_mb=64) if world > 1 else None
     if buckets is not None:
         opt.grad_scale = buckets.grad_scale
-    T = args.tokens
-    x = torch.randn(T, model.d, device=dev, dtype=torch.bfloat16)
-    flops_step = float(model.gemm_flops_per_token()) * T
 
     def step(xin):
         if buckets is not None:
             buckets.reset()
         else:
             opt.zero_grad()
-        loss = model(xin)
+        loss = fwd(xin)
         loss.backward()
         if buckets is not None:
             buckets.finish()
@@ -300,10 +319,21 @@ def main() -> None:
                 "frac_of_hbm": d["work"] / (d["ms"] / 1e3) / 1e9 / hbm}
 
     total_kernel_ms = sum(d["ms"] for d in kern.values()) / args.steps
+    llama = args.workload == "llama7b"
+    if llama:
+        wl = (f"configs[3]/[4]: Llama-2-7B-shape decoder training step (d 4096, ffn 11008, 32 heads, vocab 32000, "
+              f"{args.layers} layers, seq {T}, batch 1/GPU), MOSS FP8 linears, bf16 SDPA/norm/head, "
+              f"MossAdamW over all params")
+        if e2e is not None:
+            e2e = {**e2e, "value": world * T / (e2e["ms_per_step"] / 1e3), "unit": "tokens/s"}
+    else:
+        wl = ("configs[1]: MOSS quantize + MXFP8 fwd/dgrad/wgrad GEMMs over the Llama-7B linear "
+              "shapes (QKV 4096->12288, O 4096->4096, gate/up 4096->2x11008, down 11008->4096) "
+              "+ fused AdamW/autoscale/FP8-copy, as one training step")
     line = {
         "metric": METRIC,
-        "value": world * flops_step / (ms / 1e3) / 1e12,
-        "unit": "TFLOP/s",
+        "value": (world * T / (ms / 1e3)) if llama else world * flops_step / (ms / 1e3) / 1e12,
+        "unit": "tokens/s" if llama else "TFLOP/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": max(3, args.warmup),
@@ -313,12 +343,10 @@ def main() -> None:
         "vs_baseline": None,
         "dtype": "e4m3 x e4m3 -> fp32 accumulate (MXFP8, E8M0 block scales); bf16 activations; fp32 master/optimizer",
         "data": "synthetic (randn bf16 activations, N(0,0.02^2) weights, random init)",
-        "config": {"workload": "configs[1]: MOSS quantize + MXFP8 fwd/dgrad/wgrad GEMMs over the Llama-7B linear "
-                               "shapes (QKV 4096->12288, O 4096->4096, gate/up 4096->2x11008, down 11008->4096) "
-                               "+ fused AdamW/autoscale/FP8-copy, as one training step",
-                   "tokens_per_gpu": T, "global_batch_tokens": T * world,
+        "config": {"workload": wl, "tokens_per_gpu": T, "global_batch_tokens": T * world,
                    "parallelism": f"dp{world}" + (" (NCCL bucketed fp32 grad all-reduce)" if world > 1 else ""),
                    "gemm_flops_per_step_per_gpu": flops_step,
+                   "gemm_tflops_per_s_whole_step": world * flops_step / (ms / 1e3) / 1e12,
                    "l2": "not flushed: per-step working set ~3 GB >> 126 MB L2"},
         "tokens_per_s": world * T / (ms / 1e3),
         "gpu_launches": launches,

