@@ -118,6 +118,16 @@ int moss_adamw_fp8(float* w, const void* g, int g_dtype, float* m, float* v, int
                    const moss_adam_params* p, float enc_scale, uint8_t* w_fp8, uint8_t* w_fp8_t,
                    float* w_amax, uint32_t* n_saturated, uint32_t* flags, void* stream);
 
+/* K3 with device-resident hyper-parameters, for CUDA-graph replay: *p_dev
+ * and *enc_scale_dev are read by the kernel (the host refreshes them with a
+ * stream-ordered H2D copy before each replay).  scale_out (nullable) receives
+ * *enc_scale_dev when the update is done — the f32(s_{t+1}) the next forward's
+ * GEMMs read as the weight's per-tensor scale. */
+int moss_adamw_fp8_dev(float* w, const void* g, int g_dtype, float* m, float* v, int64_t rows, int64_t cols,
+                       const moss_adam_params* p_dev, const float* enc_scale_dev, float* scale_out,
+                       uint8_t* w_fp8, uint8_t* w_fp8_t, float* w_amax, uint32_t* n_saturated,
+                       uint32_t* flags, void* stream);
+
 /* Human-readable status. */
 const char* moss_strerror(int status);
 

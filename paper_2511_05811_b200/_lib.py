@@ -39,6 +39,7 @@ _SIGS = {
     "moss_gemm_mxf8": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _I, _P]),
     "moss_adamw_fp8": (_I, [_P, _P, _I, _P, _P, _I64, _I64, ctypes.POINTER(AdamParams), _F, _P, _P, _P,
                             _P, _P, _P]),
+    "moss_adamw_fp8_dev": (_I, [_P, _P, _I, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
 }
 
 _lib = None
@@ -214,6 +215,18 @@ def gemm(a, sfa, b, sfb, s_a, s_b, d, *, accumulate: bool = False) -> None:
                                    s_b.data_ptr(), d.data_ptr(), dtype_code(d), d.stride(0), m, n, k,
                                    int(accumulate), stream()),
               "moss_gemm_mxf8")
+
+
+def adamw_fp8_dev(w, g, m, v, rows: int, cols: int, p_dev: int, enc_dev: int | None, flags: FlagWord, *,
+                  scale_out=None, w_fp8=None, w_fp8_t=None, w_amax=None, n_saturated=None) -> None:
+    """K3 reading its hyper-parameters / encode scale from device memory (graph-capturable)."""
+    n = rows * cols
+    nbytes = n * (4 + g.element_size() + 8) + n * 12 + n * ((w_fp8 is not None) + (w_fp8_t is not None))
+    with _Span("adamw", nbytes):
+        check(lib().moss_adamw_fp8_dev(w.data_ptr(), g.data_ptr(), dtype_code(g), m.data_ptr(), v.data_ptr(), rows,
+                                       cols, p_dev, enc_dev, ptr(scale_out), ptr(w_fp8), ptr(w_fp8_t), ptr(w_amax),
+                                       ptr(n_saturated), flags.ptr, stream()),
+              "moss_adamw_fp8_dev")
 
 
 def adamw_fp8(w, g, m, v, rows: int, cols: int, params: AdamParams, enc_scale: float, flags: FlagWord, *,

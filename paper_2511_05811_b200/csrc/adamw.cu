@@ -40,8 +40,14 @@ template <typename GT, bool ENC, bool TRANS>
 __global__ void __launch_bounds__(256) adamw_fp8_kernel(float* __restrict__ w, const GT* __restrict__ g,
                                                         float* __restrict__ m, float* __restrict__ v, int64_t rows,
                                                         int64_t cols, moss_adam_params p, float enc_scale,
+                                                        const moss_adam_params* __restrict__ p_dev,
+                                                        const float* __restrict__ enc_dev, float* scale_out,
                                                         uint8_t* __restrict__ w_fp8, uint8_t* __restrict__ w_fp8_t,
                                                         float* w_amax, uint32_t* nsat, uint32_t* flags) {
+    // device-resident hyper-parameters (CUDA-graph replays): read them once per CTA
+    if (p_dev) p = *p_dev;
+    if (enc_dev) enc_scale = *enc_dev;
+    if (scale_out && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *scale_out = enc_scale;
     __shared__ __align__(16) uint8_t ctile[TRANS ? AT_ROWS : 1][AT_COLS];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t c0 = (int64_t)blockIdx.x * AT_COLS;
@@ -126,29 +132,32 @@ __global__ void __launch_bounds__(256) adamw_fp8_kernel(float* __restrict__ w, c
 
 template <typename GT>
 static void launch_adamw_t(float* w, const GT* g, float* m, float* v, int64_t rows, int64_t cols,
-                           const moss_adam_params& p, float enc_scale, uint8_t* w_fp8, uint8_t* w_fp8_t,
+                           const moss_adam_params& p, float enc_scale, const moss_adam_params* p_dev,
+                           const float* enc_dev, float* scale_out, uint8_t* w_fp8, uint8_t* w_fp8_t,
                            float* w_amax, uint32_t* nsat, uint32_t* flags, cudaStream_t st) {
     dim3 grid((unsigned)((cols + AT_COLS - 1) / AT_COLS), (unsigned)((rows + AT_ROWS - 1) / AT_ROWS));
     if (w_fp8_t)
-        adamw_fp8_kernel<GT, true, true><<<grid, 256, 0, st>>>(w, g, m, v, rows, cols, p, enc_scale, w_fp8, w_fp8_t,
-                                                               w_amax, nsat, flags);
+        adamw_fp8_kernel<GT, true, true><<<grid, 256, 0, st>>>(w, g, m, v, rows, cols, p, enc_scale, p_dev, enc_dev,
+                                                               scale_out, w_fp8, w_fp8_t, w_amax, nsat, flags);
     else if (w_fp8)
-        adamw_fp8_kernel<GT, true, false><<<grid, 256, 0, st>>>(w, g, m, v, rows, cols, p, enc_scale, w_fp8, w_fp8_t,
-                                                                w_amax, nsat, flags);
+        adamw_fp8_kernel<GT, true, false><<<grid, 256, 0, st>>>(w, g, m, v, rows, cols, p, enc_scale, p_dev, enc_dev,
+                                                                scale_out, w_fp8, w_fp8_t, w_amax, nsat, flags);
     else
-        adamw_fp8_kernel<GT, false, false><<<grid, 256, 0, st>>>(w, g, m, v, rows, cols, p, enc_scale, w_fp8,
-                                                                 w_fp8_t, w_amax, nsat, flags);
+        adamw_fp8_kernel<GT, false, false><<<grid, 256, 0, st>>>(w, g, m, v, rows, cols, p, enc_scale, p_dev, enc_dev,
+                                                                 scale_out, w_fp8, w_fp8_t, w_amax, nsat, flags);
 }
 
 int launch_adamw(float* w, const void* g, int g_dtype, float* m, float* v, int64_t rows, int64_t cols,
-                 const moss_adam_params& p, float enc_scale, uint8_t* w_fp8, uint8_t* w_fp8_t, float* w_amax,
-                 uint32_t* nsat, uint32_t* flags, cudaStream_t st) {
+                 const moss_adam_params& p, float enc_scale, const moss_adam_params* p_dev, const float* enc_dev,
+                 float* scale_out, uint8_t* w_fp8, uint8_t* w_fp8_t, float* w_amax, uint32_t* nsat,
+                 uint32_t* flags, cudaStream_t st) {
     if (w_amax && cudaMemsetAsync(w_amax, 0, sizeof(float), st) != cudaSuccess) return MOSS_ERR_CUDA;
     if (g_dtype == MOSS_BF16)
-        launch_adamw_t(w, (const __nv_bfloat16*)g, m, v, rows, cols, p, enc_scale, w_fp8, w_fp8_t, w_amax, nsat, flags,
-                       st);
+        launch_adamw_t(w, (const __nv_bfloat16*)g, m, v, rows, cols, p, enc_scale, p_dev, enc_dev, scale_out, w_fp8,
+                       w_fp8_t, w_amax, nsat, flags, st);
     else
-        launch_adamw_t(w, (const float*)g, m, v, rows, cols, p, enc_scale, w_fp8, w_fp8_t, w_amax, nsat, flags, st);
+        launch_adamw_t(w, (const float*)g, m, v, rows, cols, p, enc_scale, p_dev, enc_dev, scale_out, w_fp8, w_fp8_t,
+                       w_amax, nsat, flags, st);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 

@@ -17,8 +17,9 @@ int launch_gemm(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const ui
                 const float* sB, void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
                 cudaStream_t st);
 int launch_adamw(float* w, const void* g, int g_dtype, float* m, float* v, int64_t rows, int64_t cols,
-                 const moss_adam_params& p, float enc_scale, uint8_t* w_fp8, uint8_t* w_fp8_t, float* w_amax,
-                 uint32_t* nsat, uint32_t* flags, cudaStream_t st);
+                 const moss_adam_params& p, float enc_scale, const moss_adam_params* p_dev, const float* enc_dev,
+                 float* scale_out, uint8_t* w_fp8, uint8_t* w_fp8_t, float* w_amax, uint32_t* nsat,
+                 uint32_t* flags, cudaStream_t st);
 }  // namespace moss
 
 static inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
@@ -104,8 +105,23 @@ int moss_adamw_fp8(float* w, const void* g, int g_dtype, float* m, float* v, int
     if (!aligned(w, 16) || !aligned(g, 16) || !aligned(m, 16) || !aligned(v, 16) || (w_fp8 && !aligned(w_fp8, 8)) ||
         (w_fp8_t && !aligned(w_fp8_t, 16)))
         return MOSS_ERR_ALIGN;
-    return moss::launch_adamw(w, g, g_dtype, m, v, rows, cols, *p, enc_scale, w_fp8, w_fp8_t, w_amax, n_saturated,
-                              flags, (cudaStream_t)stream);
+    return moss::launch_adamw(w, g, g_dtype, m, v, rows, cols, *p, enc_scale, nullptr, nullptr, nullptr, w_fp8,
+                              w_fp8_t, w_amax, n_saturated, flags, (cudaStream_t)stream);
+}
+
+int moss_adamw_fp8_dev(float* w, const void* g, int g_dtype, float* m, float* v, int64_t rows, int64_t cols,
+                       const moss_adam_params* p_dev, const float* enc_scale_dev, float* scale_out, uint8_t* w_fp8,
+                       uint8_t* w_fp8_t, float* w_amax, uint32_t* n_saturated, uint32_t* flags, void* stream) {
+    if (rows <= 0 || cols <= 0 || cols % 8) return MOSS_ERR_SHAPE;
+    if (w_fp8_t && rows % 32) return MOSS_ERR_SHAPE;
+    if (!w || !g || !m || !v || !p_dev || !flags || !dtype_ok(g_dtype)) return MOSS_ERR_ARGUMENT;
+    if ((w_fp8 || w_fp8_t || scale_out) && !enc_scale_dev) return MOSS_ERR_ARGUMENT;
+    if (!aligned(w, 16) || !aligned(g, 16) || !aligned(m, 16) || !aligned(v, 16) || !aligned(p_dev, 4) ||
+        (w_fp8 && !aligned(w_fp8, 8)) || (w_fp8_t && !aligned(w_fp8_t, 16)))
+        return MOSS_ERR_ALIGN;
+    moss_adam_params dummy{};
+    return moss::launch_adamw(w, g, g_dtype, m, v, rows, cols, dummy, 1.0f, p_dev, enc_scale_dev, scale_out, w_fp8,
+                              w_fp8_t, w_amax, n_saturated, flags, (cudaStream_t)stream);
 }
 
 }  // extern "C"

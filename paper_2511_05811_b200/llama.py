@@ -168,9 +168,10 @@ class MarkovTokens:
     sparse Markov chain (each token has ``fanout`` successors with Dirichlet
     probabilities), so the loss falls from ln(V) towards the chain's entropy."""
 
-    def __init__(self, vocab: int, seed: int = 0, fanout: int = 4):
+    def __init__(self, vocab: int, seed: int = 0, fanout: int = 4, active: int | None = None):
         rng = np.random.default_rng(seed)
-        self.vocab = vocab
+        self.vocab = active or vocab       # states actually visited (<= model vocab)
+        vocab = self.vocab
         self.succ = rng.integers(0, vocab, size=(vocab, fanout))
         self.prob = rng.dirichlet(np.ones(fanout) * 0.5, size=vocab)
         self.cum = np.cumsum(self.prob, axis=1)

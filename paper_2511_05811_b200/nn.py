@@ -39,7 +39,7 @@ from .gemm import mx_gemm
 from .optim import adam_params
 from .quantize import quantize_mx2
 
-__all__ = ["MossLinearFunction", "MossLinear", "MossAdamW", "device_flags", "raise_if_flagged"]
+__all__ = ["MossLinearFunction", "MossLinear", "MossAdamW", "CudaGraphStep", "device_flags", "raise_if_flagged", "cosine_lr"]
 
 _FLAGS: dict[str, _lib.FlagWord] = {}
 
@@ -187,7 +187,18 @@ class MossAdamW:
     Other parameters (embeddings, norms, head): the same kernel, no copy.
     Gradients: ``p.main_grad`` for MossLinear weights, ``p.grad`` otherwise
     (both FP32); ``grad_scale`` multiplies them (DP averaging).
+
+    A step is ``prepare()`` (host, O(1) per parameter: the schedule advance
+    of autoscale.py:71-79, bias corrections, the per-parameter kernel
+    arguments staged in a pinned ring and sent with ONE stream-ordered H2D
+    copy) followed by ``launch()`` (the kernels, which read those arguments
+    from device memory — so ``launch`` can be captured in a CUDA graph and
+    replayed).  ``step()`` does both.  Rescale steps need the amax of the
+    updated weights on the host and run eagerly (``launch(rescale=True)``).
     """
+
+    _WORDS = 12            # moss_adam_params (9 words) + enc scale (word 9), padded to 48 B
+    _RING = 8
 
     def __init__(self, params: Iterable[nn.Parameter] | nn.Module, lr: float = 3e-4,
                  betas: tuple[float, float] = (0.9, 0.95), eps: float = 1e-8, weight_decay: float = 0.1,
@@ -200,63 +211,136 @@ class MossAdamW:
         if not (0.0 <= betas[0] < 1.0 and 0.0 <= betas[1] < 1.0):
             raise InvalidArgumentError("betas must lie in [0, 1)")
         self.params = [p for _, p in named if p.requires_grad]
+        if not self.params:
+            raise InvalidArgumentError("no trainable parameters")
         for p in self.params:
             if p.dtype != torch.float32:
                 raise InvalidArgumentError("MossAdamW keeps FP32 master parameters")
             if p.numel() % 8:
                 raise InvalidShapeError("parameter numel must be a multiple of 8")
+            layer = getattr(p, "moss_layer", None)
+            if layer is not None and layer.schedule is None:
+                layer.init_fp8()                       # schedule_from_weights at t = 0
         self.wd_of = {id(p): (0.0 if (no_decay and no_decay(n, p)) else weight_decay) for n, p in named}
         self.lr, self.betas, self.eps = lr, betas, eps
         self.lr_schedule = lr_schedule
         self.decoupled = decoupled_decay
         self.t = 0
         self.grad_scale = 1.0
+        dev = self.params[0].device
         self.state = {id(p): (torch.zeros_like(p), torch.zeros_like(p)) for p in self.params}
-        self.saturations = torch.zeros(1, dtype=torch.int32, device=self.params[0].device) if self.params else None
+        self.saturations = torch.zeros(1, dtype=torch.int32, device=dev)
         self.rescale_events: list[tuple[int, int]] = []
+        n = len(self.params)
+        self.hp_dev = torch.zeros(n * self._WORDS, dtype=torch.float32, device=dev)
+        self.hp_pinned = torch.zeros(self._RING, n * self._WORDS, dtype=torch.float32).pin_memory()
+        self._ring_events: list = [None] * self._RING
+        self._slot = 0
+        self._rescale_pending = False
 
-    def zero_grad(self) -> None:
+    def zero_grad(self, set_to_none: bool = True) -> None:
         for p in self.params:
             if hasattr(p, "moss_layer"):
                 p.grad_fresh = True
             elif p.grad is not None:
-                p.grad = None
+                if set_to_none:
+                    p.grad = None
+                else:
+                    p.grad.zero_()
 
     def current_lr(self) -> float:
         return self.lr_schedule(self.t) if self.lr_schedule is not None else self.lr
 
-    @torch.no_grad()
-    def step(self, lr: float | None = None) -> None:
+    def rescale_due_next(self) -> bool:
+        """Will the coming step end with a rescale (autoscale.py:82-83)?"""
+        for p in self.params:
+            layer = getattr(p, "moss_layer", None)
+            if layer is not None:
+                sc = layer.schedule
+                return (sc.t + 1) - sc.last_rescale_step >= sc.interval
+        return False
+
+    def prepare(self, lr: float | None = None) -> bool:
+        """Host half of a step; returns True when this step must rescale (eager launch)."""
         eta = self.current_lr() if lr is None else lr
         self.t += 1
         b1, b2 = self.betas
-        for p in self.params:
+        bc1, bc2 = 1.0 - b1 ** self.t, 1.0 - b2 ** self.t
+        slot = self._slot
+        self._slot = (slot + 1) % self._RING
+        ev = self._ring_events[slot]
+        if ev is not None:
+            ev.synchronize()                                   # the copy that last read this slot is done
+        buf = self.hp_pinned[slot].numpy().reshape(-1, self._WORDS)
+        ibuf = buf.view(np.uint32)
+        buf[:, 0] = eta
+        buf[:, 1] = b1
+        buf[:, 2] = b2
+        buf[:, 3] = self.eps
+        buf[:, 5] = bc1
+        buf[:, 6] = bc2
+        ibuf[:, 7] = int(self.decoupled)
+        buf[:, 8] = self.grad_scale
+        rescale = False
+        for i, p in enumerate(self.params):
+            buf[i, 4] = self.wd_of[id(p)]
+            layer = getattr(p, "moss_layer", None)
+            if layer is not None:
+                sched = layer.schedule
+                auto_scale_advance(sched, eta)                 # O(1), autoscale.py:71-79
+                rescale |= rescale_due(sched)
+                buf[i, 9] = np.float32(sched.s_t)
+        self.hp_dev.copy_(self.hp_pinned[slot], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._ring_events[slot] = ev
+        self._rescale_pending = rescale
+        return rescale
+
+    @torch.no_grad()
+    def launch(self, rescale: bool | None = None) -> None:
+        """Device half of a step: one fused kernel per parameter (graph-capturable when not rescaling)."""
+        rescale = self._rescale_pending if rescale is None else rescale
+        base = self.hp_dev.data_ptr()
+        stride = self._WORDS * 4
+        for i, p in enumerate(self.params):
             layer = getattr(p, "moss_layer", None)
             g = p.main_grad if layer is not None else p.grad
             if g is None:
                 continue
             m, v = self.state[id(p)]
-            hp = adam_params(eta, b1, b2, self.eps, self.wd_of[id(p)], self.t, self.decoupled, self.grad_scale)
             flags = device_flags(p.device)
+            p_dev = base + i * stride
             if layer is None:
                 rows, cols = (p.shape[0], p.shape[1]) if p.dim() == 2 and p.shape[1] % 8 == 0 else (1, p.numel())
-                _lib.adamw_fp8(p.data, g, m, v, rows, cols, hp, 0.0, flags)
+                _lib.adamw_fp8_dev(p.data, g, m, v, rows, cols, p_dev, None, flags)
+                continue
+            rows, cols = p.shape
+            if rescale:
+                _lib.adamw_fp8_dev(p.data, g, m, v, rows, cols, p_dev, None, flags, w_amax=layer.w_amax)
+            else:
+                _lib.adamw_fp8_dev(p.data, g, m, v, rows, cols, p_dev, p_dev + 36, flags, scale_out=layer.w_scale,
+                                   w_fp8=layer.w_fp8, w_fp8_t=layer.w_fp8_t, w_amax=layer.w_amax,
+                                   n_saturated=self.saturations)
+        if rescale:
+            self._finish_rescale()
+
+    def _finish_rescale(self) -> None:
+        """JIT snap of every MOSS scale to max|W'|/448 and re-encode (autoscale.py:86-96)."""
+        for p in self.params:
+            layer = getattr(p, "moss_layer", None)
+            if layer is None:
                 continue
             sched = layer.schedule
-            auto_scale_advance(sched, eta)                       # O(1), autoscale.py:71-79
-            rows, cols = p.shape
-            if rescale_due(sched):                               # autoscale.py:82-96
-                _lib.adamw_fp8(p.data, g, m, v, rows, cols, hp, 0.0, flags, w_amax=layer.w_amax)
-                amax = float(layer.w_amax.item())
-                sched.s_t = amax / E4M3.max_value if amax > 0 else 1.0
-                sched.last_rescale_step = sched.t
-                self.rescale_events.append((self.t, id(p)))
-                layer.encode_weight()
-            else:
-                s = float(np.float32(sched.s_t))
-                _lib.adamw_fp8(p.data, g, m, v, rows, cols, hp, s, flags, w_fp8=layer.w_fp8,
-                               w_fp8_t=layer.w_fp8_t, w_amax=layer.w_amax, n_saturated=self.saturations)
-                layer.w_scale.fill_(s)
+            amax = float(layer.w_amax.item())
+            sched.s_t = amax / E4M3.max_value if amax > 0 else 1.0
+            sched.last_rescale_step = sched.t
+            self.rescale_events.append((self.t, id(p)))
+            layer.encode_weight()
+        self._rescale_pending = False
+
+    def step(self, lr: float | None = None) -> None:
+        self.launch(self.prepare(lr))
 
     def check(self, where: str = "MossAdamW") -> None:
         """Raise pending device-side errors (non-finite grads/activations, E8M0 range)."""
@@ -273,6 +357,51 @@ class MossAdamW:
                 jit = float(layer.w_amax.item()) / E4M3.max_value
                 bad += int(layer.schedule.s_t < jit)
         return bad
+
+
+class CudaGraphStep:
+    """A whole training step (forward, backward, gradient exchange, fused
+    optimizer kernels) captured once in a CUDA graph and replayed.
+
+    ``step_fn(*inputs) -> loss`` must run forward + backward (+ DP finish);
+    the optimizer's device half is captured after it.  Per replay the host
+    only runs ``opt.prepare()`` (O(1) per parameter + one H2D copy) and
+    ``graph.replay()``.  Steps that end with a rescale (every ``interval``
+    steps) run eagerly, exactly like the uncaptured path.
+    """
+
+    def __init__(self, step_fn, opt: MossAdamW, static_inputs: tuple, zero_grad=None):
+        self.fn, self.opt, self.inputs = step_fn, opt, static_inputs
+        self.zero_grad = zero_grad or (lambda: opt.zero_grad(set_to_none=True))
+        self.graph = None
+        self.loss = None
+
+    def _capture(self) -> None:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        self.zero_grad()
+        with torch.cuda.graph(self.graph, stream=s):
+            self.loss = self.fn(*self.inputs)
+            self.opt.launch(False)
+        torch.cuda.current_stream().wait_stream(s)
+
+    def __call__(self, *inputs) -> torch.Tensor:
+        for dst, src in zip(self.inputs, inputs):
+            if src is not dst:
+                dst.copy_(src, non_blocking=True)
+        if self.opt.rescale_due_next() or self.graph is None:
+            # eager step (rescale, or the step before the first capture)
+            self.zero_grad()
+            loss = self.fn(*self.inputs)
+            self.opt.step()
+            if self.graph is None:
+                self._capture()
+            return loss
+        self.opt.prepare()
+        self.graph.replay()
+        return self.loss
 
 
 def cosine_lr(peak: float, warmup: int, total: int, floor_frac: float = 0.1) -> Callable[[int], float]:

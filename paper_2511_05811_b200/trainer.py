@@ -40,26 +40,42 @@ def make_optimizer(model: LlamaModel, lr: float, steps: int, warmup: int, weight
 
 def train(model: LlamaModel, data: MarkovTokens, *, steps: int, batch: int, seq: int, lr: float = 1e-3,
           warmup: int = 20, weight_decay: float = 0.1, buckets=None, divergence_threshold: float = 1e6,
-          check_every: int = 1) -> TrainLog:
+          check_every: int = 1, cuda_graph: bool = False) -> TrainLog:
+    """``cuda_graph=True`` (single GPU) captures forward + backward + the
+    optimizer kernels once and replays the graph each step (nn.CudaGraphStep)."""
     opt = make_optimizer(model, lr, steps, warmup, weight_decay)
     if buckets is not None:
         opt.grad_scale = buckets.grad_scale
     dev = next(model.parameters()).device
     log = TrainLog()
+    graphed = None
+    if cuda_graph:
+        from .nn import CudaGraphStep
+        sx = torch.zeros((batch, seq), dtype=torch.long, device=dev)
+        sy = torch.zeros((batch, seq), dtype=torch.long, device=dev)
+
+        def fb(xt, yt):
+            loss = model(xt, yt)
+            loss.backward()
+            return loss
+        graphed = CudaGraphStep(fb, opt, (sx, sy))
     for step in range(steps):
         x, y = data.batch(batch, seq)
         xt = torch.as_tensor(x, device=dev)
         yt = torch.as_tensor(y, device=dev)
-        if buckets is not None:
-            buckets.reset()
-        else:
-            opt.zero_grad()
-        loss = model(xt, yt)
-        loss.backward()
-        if buckets is not None:
-            buckets.finish()
         log.lr.append(opt.current_lr())
-        opt.step()
+        if graphed is not None:
+            loss = graphed(xt, yt)
+        else:
+            if buckets is not None:
+                buckets.reset()
+            else:
+                opt.zero_grad()
+            loss = model(xt, yt)
+            loss.backward()
+            if buckets is not None:
+                buckets.finish()
+            opt.step()
         lv = float(loss.detach())
         if step % check_every == 0:
             opt.check(f"step {step}")
