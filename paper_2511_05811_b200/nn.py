@@ -379,6 +379,13 @@ class CudaGraphStep:
     def _capture(self) -> None:
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
+        # warm-up on the capture stream (autograd / allocator state), as torch requires
+        with torch.cuda.stream(s):
+            for _ in range(2):
+                self.zero_grad()
+                self.fn(*self.inputs)
+                self.opt.step()
+        torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
         self.zero_grad()
