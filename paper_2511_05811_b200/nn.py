@@ -71,12 +71,17 @@ def _aligned_2d(x: torch.Tensor, k: int) -> torch.Tensor:
 class MossLinearFunction(torch.autograd.Function):
     """y = x W^T with MOSS FP8 forward, dgrad and wgrad (three tcgen05 GEMMs)."""
 
+    # The FP32 master weight is NOT an autograd input: its gradient is written
+    # by the wgrad GEMM straight into ``weight.main_grad`` (FP32, possibly a
+    # DP bucket view).  Keeping it out of the autograd graph also means no
+    # AccumulateGrad node (and no stream bookkeeping) exists for it, which keeps
+    # whole-step CUDA-graph capture clean.
     @staticmethod
-    def forward(ctx, x: torch.Tensor, weight: torch.Tensor, layer: "MossLinear") -> torch.Tensor:
+    def forward(ctx, x: torch.Tensor, layer: "MossLinear") -> torch.Tensor:
         k = x.shape[-1]
         n = layer.out_features
         x2d = _aligned_2d(x, k)
-        need_w = weight.requires_grad
+        need_w = layer.weight.requires_grad
         flags = device_flags(x.device)
         op = quantize_mx2(x2d, row=True, col=need_w, flags=flags)
         y = mx_gemm(op.codes, op.sf, op.g, layer.w_fp8, None, layer.w_scale, out_dtype=torch.bfloat16)
@@ -115,7 +120,7 @@ class MossLinearFunction(torch.autograd.Function):
             hook = getattr(w, "grad_ready_hook", None)
             if hook is not None:
                 hook(w)
-        return dx, None, None
+        return dx, None
 
 
 class MossLinear(nn.Module):
@@ -171,7 +176,7 @@ class MossLinear(nn.Module):
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         if self.schedule is None:
             self.init_fp8()
-        return MossLinearFunction.apply(x, self.weight, self)
+        return MossLinearFunction.apply(x, self)
 
     def extra_repr(self) -> str:
         return f"in_features={self.in_features}, out_features={self.out_features}, fp8=e4m3(mx2 act, per-tensor W)"
@@ -383,7 +388,7 @@ class CudaGraphStep:
         with torch.cuda.stream(s):
             for _ in range(2):
                 self.zero_grad()
-                self.fn(*self.inputs)
+                self.fn(*self.inputs).detach()
                 self.opt.step()
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
@@ -401,7 +406,7 @@ class CudaGraphStep:
         if self.opt.rescale_due_next() or self.graph is None:
             # eager step (rescale, or the step before the first capture)
             self.zero_grad()
-            loss = self.fn(*self.inputs)
+            loss = self.fn(*self.inputs).detach()      # drop the eager autograd graph
             self.opt.step()
             if self.graph is None:
                 self._capture()
