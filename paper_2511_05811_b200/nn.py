@@ -71,17 +71,16 @@ def _aligned_2d(x: torch.Tensor, k: int) -> torch.Tensor:
 class MossLinearFunction(torch.autograd.Function):
     """y = x W^T with MOSS FP8 forward, dgrad and wgrad (three tcgen05 GEMMs)."""
 
-    # The FP32 master weight is NOT an autograd input: its gradient is written
-    # by the wgrad GEMM straight into ``weight.main_grad`` (FP32, possibly a
-    # DP bucket view).  Keeping it out of the autograd graph also means no
-    # AccumulateGrad node (and no stream bookkeeping) exists for it, which keeps
-    # whole-step CUDA-graph capture clean.
+    # The FP32 master weight is an autograd input only so that autograd tracks
+    # the dependency; its gradient is returned as None and instead written by
+    # the wgrad GEMM straight into ``weight.main_grad`` (FP32, possibly a DP
+    # bucket view), with no extra pass over the gradient.
     @staticmethod
-    def forward(ctx, x: torch.Tensor, layer: "MossLinear") -> torch.Tensor:
+    def forward(ctx, x: torch.Tensor, weight: torch.Tensor, layer: "MossLinear") -> torch.Tensor:
         k = x.shape[-1]
         n = layer.out_features
         x2d = _aligned_2d(x, k)
-        need_w = layer.weight.requires_grad
+        need_w = weight.requires_grad
         flags = device_flags(x.device)
         op = quantize_mx2(x2d, row=True, col=need_w, flags=flags)
         y = mx_gemm(op.codes, op.sf, op.g, layer.w_fp8, None, layer.w_scale, out_dtype=torch.bfloat16)
@@ -120,7 +119,7 @@ class MossLinearFunction(torch.autograd.Function):
             hook = getattr(w, "grad_ready_hook", None)
             if hook is not None:
                 hook(w)
-        return dx, None
+        return dx, None, None
 
 
 class MossLinear(nn.Module):
@@ -176,7 +175,7 @@ class MossLinear(nn.Module):
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         if self.schedule is None:
             self.init_fp8()
-        return MossLinearFunction.apply(x, self)
+        return MossLinearFunction.apply(x, self.weight, self)
 
     def extra_repr(self) -> str:
         return f"in_features={self.in_features}, out_features={self.out_features}, fp8=e4m3(mx2 act, per-tensor W)"
