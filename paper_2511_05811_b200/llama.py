@@ -41,6 +41,7 @@ class LlamaConfig:
     moss: bool = True
     interval: int = 500
     compute_dtype: torch.dtype = torch.bfloat16
+    fp8_backward: bool = True       # False: reference semantics, full-precision backward (train.py:187-192)
 
     @property
     def head_dim(self) -> int:
@@ -76,7 +77,8 @@ def _linear(cfg: LlamaConfig, d_in: int, d_out: int, device):
     if _LINEAR_FACTORY is not None:
         return _LINEAR_FACTORY(cfg, d_in, d_out, device)
     if cfg.moss:
-        return MossLinear(d_in, d_out, device=device, interval=cfg.interval, init_std=cfg.init_std)
+        return MossLinear(d_in, d_out, device=device, interval=cfg.interval, init_std=cfg.init_std,
+                          fp8_backward=cfg.fp8_backward)
     return _BF16Linear(d_in, d_out, device, cfg.init_std)
 
 

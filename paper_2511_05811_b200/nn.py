@@ -82,14 +82,20 @@ class MossLinearFunction(torch.autograd.Function):
         x2d = _aligned_2d(x, k)
         need_w = weight.requires_grad
         flags = device_flags(x.device)
-        op = quantize_mx2(x2d, row=True, col=need_w, flags=flags)
+        fp8_bwd = layer.fp8_backward
+        op = quantize_mx2(x2d, row=True, col=need_w and fp8_bwd, flags=flags)
         y = mx_gemm(op.codes, op.sf, op.g, layer.w_fp8, None, layer.w_scale, out_dtype=torch.bfloat16)
         ctx.layer = layer
+        ctx.fp8_bwd = fp8_bwd
+        if not fp8_bwd:
+            # reference semantics (train.py:187-192): backward in full precision at the
+            # unquantized activation and the FP32 master weight
+            ctx.save_for_backward(x2d)
         ctx.need_w = need_w
         ctx.x_shape = x.shape
         ctx.x_dtype = x.dtype
         # FP8 activation stash: column-wise codes of X for wgrad (1 B/elem instead of bf16)
-        ctx.x_t = (op.codes_t, op.sf_t, op.g) if need_w else None
+        ctx.x_t = (op.codes_t, op.sf_t, op.g) if (need_w and fp8_bwd) else None
         return y.view(*x.shape[:-1], n)
 
     @staticmethod
@@ -97,6 +103,8 @@ class MossLinearFunction(torch.autograd.Function):
         layer = ctx.layer
         n = layer.out_features
         need_x = ctx.needs_input_grad[0]
+        if not ctx.fp8_bwd:
+            return MossLinearFunction._backward_fp(ctx, dy, layer, need_x)
         dy2d = _aligned_2d(dy, n)
         flags = device_flags(dy.device)
         opd = quantize_mx2(dy2d, row=need_x, col=ctx.need_w, flags=flags)
@@ -121,6 +129,28 @@ class MossLinearFunction(torch.autograd.Function):
                 hook(w)
         return dx, None, None
 
+    @staticmethod
+    def _backward_fp(ctx, dy, layer, need_x):
+        (x2d,) = ctx.saved_tensors
+        dy2d = dy.reshape(-1, layer.out_features)
+        w = layer.weight
+        dx = None
+        if need_x:
+            dx = (dy2d @ w.detach().to(dy2d.dtype)).view(ctx.x_shape).to(ctx.x_dtype)
+        if ctx.need_w:
+            gw = dy2d.t().float() @ x2d.float()
+            if getattr(w, "main_grad", None) is None or getattr(w, "grad_fresh", True):
+                if getattr(w, "main_grad", None) is None:
+                    w.main_grad = torch.empty_like(w, dtype=torch.float32)
+                w.main_grad.copy_(gw)
+            else:
+                w.main_grad.add_(gw)
+            w.grad_fresh = False
+            hook = getattr(w, "grad_ready_hook", None)
+            if hook is not None:
+                hook(w)
+        return dx, None, None
+
 
 class MossLinear(nn.Module):
     """FP8 (MOSS) linear layer, y = x W^T, no bias (Llama-style).
@@ -132,8 +162,9 @@ class MossLinear(nn.Module):
     """
 
     def __init__(self, in_features: int, out_features: int, bias: bool = False, device="cuda",
-                 interval: int = 500, init_std: float | None = 0.02):
+                 interval: int = 500, init_std: float | None = 0.02, fp8_backward: bool = True):
         super().__init__()
+        self.fp8_backward = fp8_backward   # False: the reference's full-precision backward (train.py:187-192)
         if bias:
             raise InvalidArgumentError("MossLinear has no bias (Llama-style linears)")
         if in_features % 32 or out_features % 32:
@@ -385,10 +416,9 @@ class CudaGraphStep:
         s.wait_stream(torch.cuda.current_stream())
         # warm-up on the capture stream (autograd / allocator state), as torch requires
         with torch.cuda.stream(s):
-            for _ in range(2):
+            for _ in range(2):                 # forward/backward only: no optimizer state change
                 self.zero_grad()
                 self.fn(*self.inputs).detach()
-                self.opt.step()
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
