@@ -4,10 +4,13 @@
    vs the CPU float64 reference of the same model whose linears and
    optimizer are the composed oracle (oracle/train_ref.py) — smoothed loss
    curves within a stated band;
-2. ~125M Llama (d 768, 12 layers, SwiGLU 2048, vocab 32000), 200 steps:
-   MOSS FP8 vs the same model with bf16 linears (the reference's own
-   quant-vs-fp band, test_train.py:53-60: smoothed final loss within 5 %),
-   no saturations, s_auto >= s_jit.
+2. ~125M Llama (d 768, 12 layers, SwiGLU 2048, vocab 32000), 600 steps:
+   MOSS FP8 vs the same model with bf16 linears; the reference's own
+   quant-vs-fp band is 5 % of the smoothed final loss (test_train.py:53-60),
+   the band here is 2 % (measured on B200: 0.17 % at 1000 steps / lr 6e-4,
+   0.40 % at 600 steps / lr 3e-4 / batch 32; profiles/r01_llama_parity.txt).
+   Short runs (< ~300 steps) are dominated by when each run escapes the
+   Markov-chain loss plateau and are not a meaningful band.
 """
 
 import math
@@ -87,15 +90,15 @@ def test_tiny_llama_gpu_vs_cpu_reference_loss_curve():
 
 @pytest.mark.slow
 def test_llama_125m_moss_vs_bf16_band():
-    steps, batch, seq, lr, warmup = 200, 8, 256, 1e-3, 20
+    steps, batch, seq, lr, warmup = 600, 8, 256, 6e-4, 60
     finals = {}
     for moss in (True, False):
         torch.manual_seed(0)
         cfg = L.LlamaConfig(**{**L.LLAMA_125M.__dict__, "moss": moss, "max_seq": seq})
         model = L.LlamaModel(cfg)
         log = train(model, L.MarkovTokens(cfg.vocab, seed=1, active=2048), steps=steps, batch=batch, seq=seq,
-                    lr=lr, warmup=warmup)
-        finals[moss] = float(np.mean(log.loss[-20:]))
+                    lr=lr, warmup=warmup, cuda_graph=True)
+        finals[moss] = float(log.smoothed(50)[-1])
         if moss:
             losses = log.loss
         del model
@@ -103,7 +106,7 @@ def test_llama_125m_moss_vs_bf16_band():
     gap = abs(finals[True] - finals[False]) / finals[False]
     print(f"125M: moss {finals[True]:.4f} bf16 {finals[False]:.4f} gap {gap:.4f}")
     assert losses[-1] < losses[0] * 0.7
-    assert gap <= 0.05
+    assert gap <= 0.02
 
 
 def test_cuda_graph_training_matches_eager():
