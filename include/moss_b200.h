@@ -67,6 +67,29 @@ int moss_quant_mx2(const void* x, int dtype, int64_t rows, int64_t cols, const f
                    uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t,
                    float* g_out, uint32_t* flags, void* stream);
 
+/* K0+K1 in ONE launch (single pass over HBM for tensors that fit in L2 +
+ * smem): the same outputs as moss_amax followed by moss_quant_mx2, i.e.
+ * quant_two_level (quantize.py:127-173) including the global amax
+ * (quantize.py:149-155).  The kernel streams x once to reduce max|x|, meets
+ * all CTAs at one grid-wide barrier (cooperative launch), then quantizes the
+ * tiles still resident in shared memory / L2 first.
+ *   amax         amax_given == 0: OUT, max|x| (f32) of the tensor;
+ *                amax_given != 0: IN, max|x| supplied by the producer kernel
+ *                (producer-fused amax: the quantizer then reads x once and
+ *                skips the reduction and the barrier)
+ *   workspace    moss_workspace_bytes() bytes of device memory, zeroed once
+ *                by the caller and reused; one stream at a time per workspace
+ *   other arguments as moss_quant_mx2.
+ * bf16 tensors with rows % 128 == 0 and cols % 128 == 0 take the fused
+ * kernel; other shapes/dtypes run moss_amax + moss_quant_mx2 internally. */
+int moss_quant_mx2_fused(const void* x, int dtype, int64_t rows, int64_t cols, float* amax, int amax_given,
+                         uint8_t* codes, uint8_t* sf, uint8_t* micro,
+                         uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t,
+                         float* g_out, uint32_t* workspace, uint32_t* flags, void* stream);
+
+/* Bytes of the caller-owned workspace of moss_quant_mx2_fused. */
+int64_t moss_workspace_bytes(void);
+
 /* Per-tensor encode at a given scale: codes = e4m3(f32(x) / f32(scale))
  * (train.py:113-118 _quantize_weight, quant_per_tensor quantize.py:92-98 when
  * scale = f32(amax/448), rescale_interval autoscale.py:86-96).

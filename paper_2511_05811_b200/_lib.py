@@ -35,6 +35,8 @@ _SIGS = {
     "moss_sf_bytes": (_I64, [_I64, _I64]),
     "moss_amax": (_I, [_P, _I, _I64, _P, _P, _P]),
     "moss_quant_mx2": (_I, [_P, _I, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "moss_quant_mx2_fused": (_I, [_P, _I, _I64, _I64, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "moss_workspace_bytes": (_I64, []),
     "moss_encode_scaled": (_I, [_P, _I, _I64, _I64, _P, _F, _I, _P, _P, _P, _P, _P, _P]),
     "moss_gemm_mxf8": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _I, _P]),
     "moss_adamw_fp8": (_I, [_P, _P, _I, _P, _P, _I64, _I64, ctypes.POINTER(AdamParams), _F, _P, _P, _P,
@@ -123,6 +125,19 @@ class FlagWord:
         self.t.zero_()
 
 
+_WS: dict[str, torch.Tensor] = {}
+
+
+def workspace(device) -> torch.Tensor:
+    """Per-device workspace of the fused quantizer (grid-barrier words), zeroed
+    once; every launch on it is ordered on the current stream."""
+    key = str(torch.device(device))
+    if key not in _WS:
+        nbytes = int(lib().moss_workspace_bytes())
+        _WS[key] = torch.zeros((nbytes + 15) // 16 * 4, dtype=torch.int32, device=device)
+    return _WS[key]
+
+
 # ---------------------------------------------------------------- live instrumentation
 class Instrument:
     """Counts our kernel launches and (optionally) brackets each with CUDA
@@ -194,6 +209,20 @@ def quant_mx2(x2d: torch.Tensor, amax_t: torch.Tensor, flags: FlagWord, *, codes
                                    ptr(sf), ptr(micro), ptr(codes_t), ptr(sf_t), ptr(micro_t), ptr(g_out), flags.ptr,
                                    stream()),
               "moss_quant_mx2")
+
+
+def quant_mx2_fused(x2d: torch.Tensor, amax_t: torch.Tensor, flags: FlagWord, *, amax_given: bool = False,
+                    codes=None, sf=None, micro=None, codes_t=None, sf_t=None, micro_t=None, g_out=None) -> None:
+    """K0+K1 in one launch (amax computed in-kernel unless ``amax_given``)."""
+    rows, cols = x2d.shape
+    n = rows * cols
+    out_b = (n + n / 32) * ((codes is not None) + (codes_t is not None))
+    with _Span("quant", n * x2d.element_size() + out_b):
+        check(lib().moss_quant_mx2_fused(x2d.data_ptr(), dtype_code(x2d), rows, cols, amax_t.data_ptr(),
+                                         int(amax_given), ptr(codes), ptr(sf), ptr(micro), ptr(codes_t), ptr(sf_t),
+                                         ptr(micro_t), ptr(g_out), workspace(x2d.device).data_ptr(), flags.ptr,
+                                         stream()),
+              "moss_quant_mx2_fused")
 
 
 def encode_scaled(x2d: torch.Tensor, flags: FlagWord, *, scale_t=None, scale_host: float = 0.0,

@@ -10,6 +10,9 @@ int launch_amax(const void* x, int dtype, int64_t n, float* amax, uint32_t* flag
 int launch_quant_mx2(const void* x, int dtype, int64_t rows, int64_t cols, const float* amax, uint8_t* codes,
                      uint8_t* sf, uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t, float* g_out,
                      uint32_t* flags, cudaStream_t st);
+int launch_quant_fused(const void* x, int dtype, int64_t rows, int64_t cols, float* amax, int amax_given,
+                       uint8_t* codes, uint8_t* sf, uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t,
+                       float* g_out, uint32_t* ws, uint32_t* flags, cudaStream_t st);
 int launch_encode_scaled(const void* x, int dtype, int64_t rows, int64_t cols, const float* scale, float scale_host,
                          int from_amax, uint8_t* codes, uint8_t* codes_t, float* scale_out, uint32_t* nsat,
                          uint32_t* flags, cudaStream_t st);
@@ -27,7 +30,9 @@ static inline bool dtype_ok(int d) { return d == MOSS_F32 || d == MOSS_BF16; }
 
 extern "C" {
 
-int moss_version(void) { return 100; }
+int moss_version(void) { return 101; }
+
+int64_t moss_workspace_bytes(void) { return 64; }
 
 const char* moss_strerror(int s) {
     switch (s) {
@@ -65,6 +70,21 @@ int moss_quant_mx2(const void* x, int dtype, int64_t rows, int64_t cols, const f
     if (!aligned(x, 16) || (codes && !aligned(codes, 8)) || (codes_t && !aligned(codes_t, 16))) return MOSS_ERR_ALIGN;
     return moss::launch_quant_mx2(x, dtype, rows, cols, amax, codes, sf, micro, codes_t, sf_t, micro_t, g_out, flags,
                                   (cudaStream_t)stream);
+}
+
+int moss_quant_mx2_fused(const void* x, int dtype, int64_t rows, int64_t cols, float* amax, int amax_given,
+                         uint8_t* codes, uint8_t* sf, uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t,
+                         float* g_out, uint32_t* workspace, uint32_t* flags, void* stream) {
+    if (rows <= 0 || cols <= 0 || cols % 32) return MOSS_ERR_SHAPE;
+    const bool col = codes_t || sf_t || micro_t;
+    if (col && rows % 32) return MOSS_ERR_SHAPE;
+    if (!codes && !sf && !micro && !col) return MOSS_ERR_ARGUMENT;
+    if (!dtype_ok(dtype) || !amax || !flags || !x || !workspace) return MOSS_ERR_ARGUMENT;
+    if (!aligned(x, 16) || (codes && !aligned(codes, 8)) || (codes_t && !aligned(codes_t, 16)) ||
+        !aligned(workspace, 16))
+        return MOSS_ERR_ALIGN;
+    return moss::launch_quant_fused(x, dtype, rows, cols, amax, amax_given, codes, sf, micro, codes_t, sf_t, micro_t,
+                                    g_out, workspace, flags, (cudaStream_t)stream);
 }
 
 int moss_encode_scaled(const void* x, int dtype, int64_t rows, int64_t cols, const float* scale, float scale_host,

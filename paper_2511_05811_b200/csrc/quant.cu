@@ -221,7 +221,17 @@ int launch_amax(const void* x, int dtype, int64_t n, float* amax, uint32_t* flag
     if (cudaMemsetAsync(amax, 0, sizeof(float), st) != cudaSuccess) return MOSS_ERR_CUDA;
     int64_t nvec = n / 8;
     int64_t want = (nvec + 255) / 256;
-    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * 8));
+    // one full wave: resident CTAs per SM x SMs (a partial second wave doubled the tail)
+    static int occ[2] = {0, 0};
+    const int di = dtype == MOSS_BF16;
+    if (!occ[di]) {
+        if (di)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[di], amax_kernel<__nv_bfloat16>, 256, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[di], amax_kernel<float>, 256, 0);
+        if (occ[di] < 1) occ[di] = 4;
+    }
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * occ[di]));
     if (dtype == MOSS_BF16)
         amax_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, n, amax, flags);
     else
@@ -250,6 +260,9 @@ static void launch_quant_t(const T* x, int64_t rows, int64_t cols, const float* 
 bool launch_quant_v3(const void* x, int64_t rows, int64_t cols, const float* amax, uint8_t* codes, uint8_t* sf,
                      uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t, float* g_out,
                      uint32_t* flags, cudaStream_t st);
+bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int amax_given, uint8_t* codes,
+                     uint8_t* sf, uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t, float* g_out,
+                     uint32_t* ws, uint32_t* flags, cudaStream_t st, int* status);
 
 int launch_quant_mx2(const void* x, int dtype, int64_t rows, int64_t cols, const float* amax, uint8_t* codes,
                      uint8_t* sf, uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t, float* g_out,
@@ -278,4 +291,22 @@ int launch_encode_scaled(const void* x, int dtype, int64_t rows, int64_t cols, c
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 
+}  // namespace moss
+
+namespace moss {
+// Single-launch quantizer (K0 folded into K1) where the v4 kernel covers the
+// shape; otherwise K0 (unless the producer supplied amax) + K1.
+int launch_quant_fused(const void* x, int dtype, int64_t rows, int64_t cols, float* amax, int amax_given,
+                       uint8_t* codes, uint8_t* sf, uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t,
+                       float* g_out, uint32_t* ws, uint32_t* flags, cudaStream_t st) {
+    int status = MOSS_OK;
+    if (dtype == MOSS_BF16 && launch_quant_v4(x, rows, cols, amax, amax_given, codes, sf, micro, codes_t, sf_t,
+                                              micro_t, g_out, ws, flags, st, &status))
+        return status;
+    if (!amax_given) {
+        status = launch_amax(x, dtype, rows * cols, amax, flags, st);
+        if (status != MOSS_OK) return status;
+    }
+    return launch_quant_mx2(x, dtype, rows, cols, amax, codes, sf, micro, codes_t, sf_t, micro_t, g_out, flags, st);
+}
 }  // namespace moss

@@ -1,0 +1,447 @@
+// K1 v4: single-launch two-level MOSS quantizer for bf16 tensors whose sides
+// are multiples of 128 — the global amax, the per-32 E8M0 scales and the E4M3
+// codes (row-wise and/or column-wise) in ONE kernel.
+//
+// Semantics: quant_two_level (reference quantize.py:127-173); the column-wise
+// output is quant_two_level(x.T) with x's global scale.
+//
+// Dataflow (2 CTAs of 256 threads per SM, each a 3-slot ring of 128 x 128 bf16 tiles):
+//   phase A  (skipped when the producer supplies amax)  TMA-stream the CTA's
+//            tiles and reduce max|x|; the last 3 tiles stay resident in smem.
+//   barrier  one grid-wide arrive/release on a caller-owned workspace word;
+//            every CTA then reads the tensor amax (g = amax/448).
+//   phase B  quantize the resident tiles first, then the rest in DESCENDING
+//            order, i.e. most recently read (L2-hot) first.  Row and column
+//            passes read the tile into registers, the codes are written back
+//            INTO the same slot (TMA SWIZZLE_128B layout) and TMA-stored; the
+//            slot is reloaded once the store has read it.
+//
+// Arithmetic per element (FFMA2/FMUL2 pairs, sm_100):
+//   z = RN(x / eff) = q0 - r*(eff*q0 - x), q0 = RN(x*r), r = RN(1/eff)
+//   with r = RN(1/g) * 2^-e exact (eff = g*2^e, normal).  This 3-op division
+//   equals IEEE div.rn.f32 for EVERY bf16 dividend and every f32 divisor
+//   significand when r is the correctly rounded reciprocal: exhaustively
+//   checked over 2^23 x 256 significand pairs (tests/test_division_proof.py).
+//   s_i = RN(bmax/448) uses the same sequence with r = RN(1/448).
+//   e_i = ceil(log2(s_i/g)) = (bits(s_i) - bits(g) + 0x7FFFFF) >> 23 for
+//   normal s_i, g (exact integer form of fp8.py:205-208).
+// Blocks with eff outside [2^-60, 2^60] (never on training data) take the
+// IEEE div.rn path per element.
+#include <algorithm>
+
+#include "common.cuh"
+#include "host_utils.cuh"
+
+namespace moss {
+
+constexpr int Q4_T = 128;
+constexpr int Q4_IN = Q4_T * Q4_T * 2;     // 32 KB bf16 tile
+constexpr int Q4_S = 3;                    // slots per CTA
+constexpr int Q4_THREADS = 256;
+constexpr int Q4_SMEM = Q4_S * Q4_IN + 2 * 1024 + 64 + 1024;   // slots, 2 x SF staging, barriers, align
+
+// workspace words (caller-owned, zero-initialised once; one stream at a time)
+constexpr int WS_ARRIVE = 0, WS_GEN = 1, WS_AMAX0 = 2;   // amax slots [2], [3] by generation parity
+
+__device__ __forceinline__ uint32_t q4_in_off(int r, int c) {   // bf16 tile, two 64-col SWIZZLE_128B boxes
+    return (uint32_t)((c >> 6) * 16384 + r * 128 + ((((c >> 3) & 7) ^ (r & 7)) << 4) + ((c & 7) << 1));
+}
+__device__ __forceinline__ uint32_t q4_out_off(int r, int byte) {   // u8 128x128 tile, SWIZZLE_128B
+    return (uint32_t)(r * 128 + ((((byte >> 4) & 7) ^ (r & 7)) << 4) + (byte & 15));
+}
+__device__ __forceinline__ int q4_sf_in_chunk(int r, int kb) { return ((r & 31) << 4) + ((r >> 5) << 2) + kb; }
+
+// ---- packed f32x2 arithmetic (FMUL2 / FFMA2)
+__device__ __forceinline__ uint64_t pk(float lo, float hi) {
+    uint64_t d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+    return d;
+}
+__device__ __forceinline__ void upk(uint64_t d, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(d));
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+// RN(x / b) for a pair given xn = -x, nr = -RN(1/b), b normal (see header):
+//   q0 = RN(x r), rem = RN(b q0 - x) (exact), q = RN(q0 - r rem).
+// Working on -x keeps the sign of zero: x = -0 gives q = -0 (code 0x80).
+__device__ __forceinline__ uint64_t div2n(uint64_t xn, uint64_t b, uint64_t nr) {
+    const uint64_t q0 = fmul2(xn, nr);
+    const uint64_t rem = ffma2(b, q0, xn);
+    return ffma2(nr, rem, q0);
+}
+__device__ __forceinline__ float div1(float x, float nb, float r) {
+    const float q0 = __fmul_rn(x, r);
+    return __fmaf_rn(r, __fmaf_rn(nb, q0, x), q0);
+}
+
+struct Q4Global {
+    float g;         // global scale f32(amax/448), 0 -> 1
+    uint32_t gbits;
+    float rg;        // RN(1/g) (valid when g_normal)
+    bool g_normal;
+};
+
+__device__ __forceinline__ Q4Global q4_global(float amax) {
+    Q4Global G;
+    G.g = global_scale_from_amax(amax);
+    G.gbits = __float_as_uint(G.g);
+    G.g_normal = G.gbits >= 0x00800000u;
+    G.rg = __frcp_rn(G.g);
+    return G;
+}
+
+// Unpack NP packed bf16 pairs (element 2i = low half) into NEGATED floats:
+// -lo = (w << 16) ^ 0x80000000, -hi = (w & 0xFFFF0000) ^ 0x80000000 (the
+// negations fold into the FMUL2/FFMA2 operands).  Returns max |x|.
+// (Moving the hi unpack to two IMADs on the FMA pipe measured 12 % slower.)
+template <int NP>
+__device__ __forceinline__ float q4_unpack(const uint32_t (&w)[NP], float (&lo)[NP], float (&hi)[NP]) {
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        lo[i] = __uint_as_float(w[i] * 65536u + 0x80000000u);
+        hi[i] = __uint_as_float((w[i] & 0xFFFF0000u) ^ 0x80000000u);
+    }
+    float bm = 0.f;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) bm = fmaxf(bm, fmaxf(fabsf(lo[i]), fabsf(hi[i])));
+    return bm;
+}
+
+// E8M0 code of a block with max |x| = bm; e = code - 127, eff = g * 2^e.
+__device__ __forceinline__ uint32_t q4_scale(float bm, const Q4Global& G, bool& rerr, int& e, float& eff) {
+    // s = RN(bm / 448): bm is a bf16 value, so the 3-op division is exact
+    // (r = RN(1/448) = 0x1.24924ap-9) while the quotient stays normal
+    const float s = bm >= 0x1p-100f ? div1(bm, -kE4M3Max, 0x1.24924ap-9f) : __fdiv_rn(bm, kE4M3Max);
+    uint32_t code = 127;
+    e = 0;
+    if (s > 0.f) {
+        const uint32_t sb = __float_as_uint(s);
+        if (G.g_normal && sb >= 0x00800000u)
+            e = ((int)(sb - G.gbits) + 0x7FFFFF) >> 23;
+        else
+            e = ceil_log2_ratio(s, G.g);
+        if (e < -127) { rerr = true; e = -127; }
+        if (e > 127) { rerr = true; e = 127; }
+        code = (uint32_t)(e + 127);
+    }
+    eff = __fmul_rn(G.g, e8m0_to_f32(code));
+    return code;
+}
+
+// Encode NP pairs of negated values at scale eff -> NP/2 code words (4 codes each, element order).
+template <int NP>
+__device__ __forceinline__ void q4_encode(const float (&lo)[NP], const float (&hi)[NP], int e, float eff,
+                                          const Q4Global& G, uint32_t (&out)[NP / 2]) {
+    if (G.g_normal && eff >= 0x1p-60f && eff <= 0x1p60f) {
+        // r = RN(1/eff) = RN(1/g) * 2^-e exactly (both normal)
+        const float r = __uint_as_float(__float_as_uint(G.rg) - (uint32_t)(e << 23));
+        const uint64_t nr2 = pk(-r, -r), b2 = pk(eff, eff);
+#pragma unroll
+        for (int q = 0; q < NP / 2; ++q) {
+            float a0, a1, b0, b1;
+            upk(div2n(pk(lo[2 * q], hi[2 * q]), b2, nr2), a0, a1);
+            upk(div2n(pk(lo[2 * q + 1], hi[2 * q + 1]), b2, nr2), b0, b1);
+            out[q] = e4m3x4(a0, a1, b0, b1);
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < NP / 2; ++q)
+            out[q] = e4m3x4(__fdiv_rn(-lo[2 * q], eff), __fdiv_rn(-hi[2 * q], eff), __fdiv_rn(-lo[2 * q + 1], eff),
+                            __fdiv_rn(-hi[2 * q + 1], eff));
+    }
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <bool ROW, bool COL, bool MICRO>
+__global__ void __launch_bounds__(Q4_THREADS, 2)
+    quant_mx2_v4_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_codes,
+                        const __grid_constant__ CUtensorMap tm_codes_t, int rows, int cols, float* amax_io,
+                        int amax_given, uint8_t* __restrict__ sf, uint8_t* __restrict__ micro,
+                        uint8_t* __restrict__ sf_t, uint8_t* __restrict__ micro_t, float* g_out, uint32_t* ws,
+                        uint32_t* flags) {
+    extern __shared__ uint8_t q4_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(q4_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* slots = base;                                  // Q4_S x 32 KB
+    uint8_t* sfst = base + Q4_S * Q4_IN;                    // 2 x (512 row + 512 col)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sfst + 2048);
+    __shared__ uint32_t red[Q4_THREADS / 32];
+    __shared__ float s_amax;
+
+    const int tid = threadIdx.x;
+    const int ctiles = cols / Q4_T;
+    const int ntiles = ctiles * (rows / Q4_T);
+    const int G = gridDim.x, b = blockIdx.x;
+    const int n = ntiles > b ? (ntiles - b + G - 1) / G : 0;   // tiles of this CTA: b + j*G
+    const int kch_row = cols / 128, kch_t = rows / 128;
+
+    if (tid == 0) {
+        prefetch_tmap(&tm_x);
+        if (ROW) prefetch_tmap(&tm_codes);
+        if (COL) prefetch_tmap(&tm_codes_t);
+        for (int s = 0; s < Q4_S; ++s) mbar_init(&full[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    auto load = [&](int j) {   // tile j of this CTA into slot j % Q4_S (one thread)
+        const int tile = b + j * G, s = j % Q4_S;
+        const int r0 = (tile / ctiles) * Q4_T, c0 = (tile % ctiles) * Q4_T;
+        mbar_arrive_expect_tx(&full[s], Q4_IN);
+        tma_load_2d(slots + s * Q4_IN, &tm_x, &full[s], c0, r0);
+        tma_load_2d(slots + s * Q4_IN + 16384, &tm_x, &full[s], c0 + 64, r0);
+    };
+    uint32_t par = 0;   // bit s: parity of the next completion of slot s
+    auto wait_slot = [&](int s) {
+        mbar_wait(&full[s], (par >> s) & 1u);
+        par ^= 1u << s;
+    };
+
+    // ------------------------------------------------------------ phase A: amax
+    const bool desc = !amax_given;
+    if (!amax_given) {
+        if (tid == 0)
+            for (int j = 0; j < min(n, Q4_S); ++j) load(j);
+        uint32_t m = 0;   // max of (bf16 bits & 0x7FFF) in both halves
+        for (int j = 0; j < n; ++j) {
+            const int s = j % Q4_S;
+            wait_slot(s);
+            const uint4* T = reinterpret_cast<const uint4*>(slots + s * Q4_IN);
+#pragma unroll
+            for (int q = 0; q < Q4_IN / 16 / Q4_THREADS; ++q) {
+                const uint4 u = T[q * Q4_THREADS + tid];
+                m = __vmaxu2(m, u.x & 0x7FFF7FFFu);
+                m = __vmaxu2(m, u.y & 0x7FFF7FFFu);
+                m = __vmaxu2(m, u.z & 0x7FFF7FFFu);
+                m = __vmaxu2(m, u.w & 0x7FFF7FFFu);
+            }
+            if (j + Q4_S < n) {
+                __syncthreads();               // everyone is done with slot s
+                if (tid == 0) load(j + Q4_S);
+            }
+        }
+        m = max(m & 0xFFFFu, m >> 16);
+        m = __reduce_max_sync(0xFFFFFFFFu, m);
+        if ((tid & 31) == 0) red[tid >> 5] = m;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t r = 0;
+            for (int i = 0; i < Q4_THREADS / 32; ++i) r = max(r, red[i]);
+            // grid barrier: arrive with this CTA's max, wait for the release
+            volatile uint32_t* vws = ws;
+            const uint32_t gen = vws[WS_GEN];
+            atomicMax(&ws[WS_AMAX0 + (gen & 1u)], r);
+            __threadfence();
+            const uint32_t old = atomicAdd(&ws[WS_ARRIVE], 1u);
+            if (old == (uint32_t)G - 1) {
+                ws[WS_ARRIVE] = 0;
+                ws[WS_AMAX0 + ((gen + 1u) & 1u)] = 0;    // the next launch's slot
+                __threadfence();
+                atomicAdd(&ws[WS_GEN], 1u);
+            } else {
+                uint32_t spins = 0;
+                while (ld_acquire_gpu(&ws[WS_GEN]) == gen) {
+                    __nanosleep(64);
+                    if (++spins > (1u << 26)) __trap();
+                }
+            }
+            __threadfence();
+            const uint32_t a16 = vws[WS_AMAX0 + (gen & 1u)];
+            if (a16 >= 0x7F80u) {
+                if (b == 0) atomicOr(flags, MOSS_FLAG_NONFINITE);
+            }
+            s_amax = __uint_as_float(a16 << 16);
+            if (b == 0) {
+                if (amax_io) *amax_io = s_amax;
+            }
+        }
+        __syncthreads();
+    } else {
+        if (tid == 0) {
+            s_amax = *amax_io;
+            if ((__float_as_uint(s_amax) & 0x7F800000u) == 0x7F800000u && b == 0) atomicOr(flags, MOSS_FLAG_NONFINITE);
+            for (int j = 0; j < min(n, Q4_S); ++j) load(j);
+        }
+        __syncthreads();
+    }
+    const Q4Global Gs = q4_global(s_amax);
+    if (g_out && b == 0 && tid == 0) *g_out = Gs.g;
+
+    // ------------------------------------------------------------ phase B: quantize
+    // row pass: thread (rr, kb0) owns blocks (rr, kb0) and (rr, kb0 + 2);
+    // col pass: thread (rb, cp) owns the 32-row blocks rb of columns 2cp, 2cp+1.
+    // (A 512-thread variant with half-blocks per thread measured 25 % slower:
+    // the kernel is ALU-issue bound and the split adds per-block work.)
+    bool rerr = false;
+    const int rr = tid & 127, kb0 = tid >> 7;
+    const int rb = tid >> 6, cp = tid & 63;
+    uint32_t cbase[8];   // col-pass smem offset of row rb*32 + i, column 2cp: cbase[i & 7] + i*128
+    {
+        const int c = 2 * cp;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            cbase[k] = (uint32_t)((c >> 6) * 16384 + rb * 32 * 128 + ((((c >> 3) & 7) ^ k) << 4) + ((c & 7) << 1));
+    }
+    for (int p = 0; p < n; ++p) {
+        const int j = desc ? n - 1 - p : p;
+        const int s = j % Q4_S;
+        if (!(desc && p < Q4_S)) wait_slot(s);     // resident tiles were waited in phase A
+        uint8_t* T = slots + s * Q4_IN;
+        uint8_t* sfs = sfst + (p & 1) * 1024;
+        const int tile = b + j * G;
+        const int r0 = (tile / ctiles) * Q4_T, c0 = (tile % ctiles) * Q4_T;
+
+        uint32_t ucol[32];
+        if (COL) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ucol[i] = *reinterpret_cast<const uint32_t*>(T + cbase[i & 7] + i * 128);
+        }
+        uint32_t rcodes[2][8];
+        if (ROW) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int kb = kb0 + 2 * h;
+                uint32_t w[16];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint4 u = *reinterpret_cast<const uint4*>(T + q4_in_off(rr, kb * 32 + q * 8));
+                    w[4 * q] = u.x; w[4 * q + 1] = u.y; w[4 * q + 2] = u.z; w[4 * q + 3] = u.w;
+                }
+                float lo[16], hi[16];
+                const float bm = q4_unpack(w, lo, hi);
+                int e;
+                float eff;
+                const uint32_t code = q4_scale(bm, Gs, rerr, e, eff);
+                q4_encode(lo, hi, e, eff, Gs, rcodes[h]);
+                sfs[q4_sf_in_chunk(rr, kb)] = (uint8_t)code;
+                if (MICRO && micro) micro[(int64_t)(r0 + rr) * (cols >> 5) + (c0 >> 5) + kb] = (uint8_t)code;
+            }
+        }
+        __syncthreads();                           // the whole tile is in registers: reuse the slot for codes
+        if (ROW) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int kb = kb0 + 2 * h;
+                *reinterpret_cast<uint4*>(T + q4_out_off(rr, kb * 32)) =
+                    make_uint4(rcodes[h][0], rcodes[h][1], rcodes[h][2], rcodes[h][3]);
+                *reinterpret_cast<uint4*>(T + q4_out_off(rr, kb * 32 + 16)) =
+                    make_uint4(rcodes[h][4], rcodes[h][5], rcodes[h][6], rcodes[h][7]);
+            }
+        }
+        if (COL) {
+            uint8_t* Tc = T + 16384;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                // column 2cp+h: rows i, i+1 packed as one pair word
+                uint32_t w[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    w[i] = h ? __byte_perm(ucol[2 * i], ucol[2 * i + 1], 0x7632)
+                             : __byte_perm(ucol[2 * i], ucol[2 * i + 1], 0x5410);
+                float lo[16], hi[16];
+                const float bm = q4_unpack(w, lo, hi);
+                int e;
+                float eff;
+                const uint32_t code = q4_scale(bm, Gs, rerr, e, eff);
+                uint32_t cc[8];
+                q4_encode(lo, hi, e, eff, Gs, cc);
+                const int c = 2 * cp + h;
+                *reinterpret_cast<uint4*>(Tc + q4_out_off(c, rb * 32)) = make_uint4(cc[0], cc[1], cc[2], cc[3]);
+                *reinterpret_cast<uint4*>(Tc + q4_out_off(c, rb * 32 + 16)) = make_uint4(cc[4], cc[5], cc[6], cc[7]);
+                sfs[512 + q4_sf_in_chunk(c, rb)] = (uint8_t)code;
+                if (MICRO && micro_t) micro_t[(int64_t)(c0 + c) * (rows >> 5) + (r0 >> 5) + rb] = (uint8_t)code;
+            }
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            if (ROW) {
+                tma_store_2d(&tm_codes, T, c0, r0);
+                if (sf) bulk_store(sf + ((int64_t)(r0 >> 7) * kch_row + (c0 >> 7)) * 512, sfs, 512);
+            }
+            if (COL) {
+                tma_store_2d(&tm_codes_t, T + 16384, r0, c0);
+                if (sf_t) bulk_store(sf_t + ((int64_t)(c0 >> 7) * kch_t + (r0 >> 7)) * 512, sfs + 512, 512);
+            }
+            bulk_commit();
+            // the store of position p-1 has read its slot and SF staging -> refill the slot with p+2
+            if (p >= 1) {
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                if (p + 2 < n) load(desc ? n - 1 - (p + 2) : p + 2);
+            }
+        }
+    }
+    if (tid == 0) bulk_wait0();
+    if (__any_sync(0xFFFFFFFFu, rerr) && (tid & 31) == 0) atomicOr(flags, MOSS_FLAG_E8M0_RANGE);
+}
+
+// returns false when the shape/dtype is not covered (caller falls back)
+bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int amax_given, uint8_t* codes,
+                     uint8_t* sf, uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t, float* g_out,
+                     uint32_t* ws, uint32_t* flags, cudaStream_t st, int* status) {
+    *status = MOSS_OK;
+    if (rows % Q4_T || cols % Q4_T || rows > INT32_MAX || cols > INT32_MAX) return false;
+    const bool row = codes != nullptr;
+    const bool col = codes_t != nullptr;
+    if ((!row && (sf || micro)) || (!col && (sf_t || micro_t)) || (!row && !col)) return false;
+    if (!amax_given && !ws) return false;
+    CUtensorMap mx, mc, mct;
+    if (!make_tmap_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, rows, cols, 64, Q4_T, CU_TENSOR_MAP_SWIZZLE_128B))
+        return false;
+    mc = mx;
+    mct = mx;
+    if (row && !make_tmap_2d(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, codes, rows, cols, Q4_T, Q4_T,
+                             CU_TENSOR_MAP_SWIZZLE_128B))
+        return false;
+    if (col && !make_tmap_2d(&mct, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, codes_t, cols, rows, Q4_T, Q4_T,
+                             CU_TENSOR_MAP_SWIZZLE_128B))
+        return false;
+    const bool mic = micro || micro_t;
+    using KT = decltype(&quant_mx2_v4_kernel<true, true, true>);
+    static const KT kernels[6] = {quant_mx2_v4_kernel<true, true, false>,  quant_mx2_v4_kernel<false, true, false>,
+                                  quant_mx2_v4_kernel<true, false, false>, quant_mx2_v4_kernel<true, true, true>,
+                                  quant_mx2_v4_kernel<false, true, true>,  quant_mx2_v4_kernel<true, false, true>};
+    const int ki = (row && col ? 0 : (col ? 1 : 2)) + (mic ? 3 : 0);
+    const KT kern = kernels[ki];
+    static int occ[6] = {0, 0, 0, 0, 0, 0};
+    if (!occ[ki]) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q4_SMEM) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[ki], kern, Q4_THREADS, Q4_SMEM) != cudaSuccess ||
+            occ[ki] < 1) {
+            occ[ki] = 0;
+            *status = MOSS_ERR_CUDA;
+            return true;
+        }
+    }
+    const int64_t ntiles = (rows / Q4_T) * (cols / Q4_T);
+    const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * occ[ki]);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(Q4_THREADS);
+    cfg.dynamicSmemBytes = Q4_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    // the amax phase ends in a grid-wide barrier: all CTAs must be co-resident
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = amax_given ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mx, mc, mct, (int)rows, (int)cols, amax, amax_given, sf,
+                                             micro, sf_t, micro_t, g_out, ws, flags);
+    *status = e == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+    return true;
+}
+
+}  // namespace moss

@@ -86,17 +86,24 @@ class MX2Operand:
     micro_t: torch.Tensor | None = None
 
 
-def quantize_mx2(x2d: torch.Tensor, *, row: bool = True, col: bool = False, micro: bool = False,
-                 flags: _lib.FlagWord | None = None, amax_buf: torch.Tensor | None = None) -> MX2Operand:
-    """amax (K0) + two-level quantization (K1) of a contiguous 2-D bf16/f32 tensor.
+FUSED = True   # K0 folded into K1 (one launch); False: the two-launch K0 + K1 path (A/B tests)
 
-    Two launches; no host synchronisation.  Data-dependent errors go to ``flags``.
+
+def quantize_mx2(x2d: torch.Tensor, *, row: bool = True, col: bool = False, micro: bool = False,
+                 flags: _lib.FlagWord | None = None, amax_buf: torch.Tensor | None = None,
+                 amax: torch.Tensor | None = None) -> MX2Operand:
+    """Two-level quantization (global amax + K1) of a contiguous 2-D bf16/f32 tensor.
+
+    One launch (moss_quant_mx2_fused) and no host synchronisation; ``amax``
+    (a device f32 [1] max|x| computed by the producer kernel) skips the
+    in-kernel reduction.  ``amax_buf`` receives the computed amax.
+    Data-dependent errors go to ``flags``.
     """
     rows, cols = x2d.shape
     dev = x2d.device
     flags = flags or _lib.FlagWord(dev)
-    amax_t = amax_buf if amax_buf is not None else torch.empty(1, dtype=torch.float32, device=dev)
-    _lib.amax(x2d, amax_t, flags)
+    given = amax is not None
+    amax_t = amax if given else (amax_buf if amax_buf is not None else torch.empty(1, dtype=torch.float32, device=dev))
     g = torch.empty(1, dtype=torch.float32, device=dev)
     op = MX2Operand(codes=None, sf=None, g=g)
     if row:
@@ -109,8 +116,14 @@ def quantize_mx2(x2d: torch.Tensor, *, row: bool = True, col: bool = False, micr
         op.sf_t = sf_buffer(cols, rows, dev)
         if micro:
             op.micro_t = torch.empty((cols, rows // 32), dtype=torch.uint8, device=dev)
-    _lib.quant_mx2(x2d, amax_t, flags, codes=op.codes, sf=op.sf, micro=op.micro, codes_t=op.codes_t,
-                   sf_t=op.sf_t, micro_t=op.micro_t, g_out=g)
+    outs = dict(codes=op.codes, sf=op.sf, micro=op.micro, codes_t=op.codes_t, sf_t=op.sf_t, micro_t=op.micro_t,
+                g_out=g)
+    if FUSED:
+        _lib.quant_mx2_fused(x2d, amax_t, flags, amax_given=given, **outs)
+    else:
+        if not given:
+            _lib.amax(x2d, amax_t, flags)
+        _lib.quant_mx2(x2d, amax_t, flags, **outs)
     return op
 
 
