@@ -151,6 +151,37 @@ int moss_adamw_fp8_dev(float* w, const void* g, int g_dtype, float* m, float* v,
                        uint8_t* w_fp8, uint8_t* w_fp8_t, float* w_amax, uint32_t* n_saturated,
                        uint32_t* flags, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Producer kernels (bf16): the Llama ops that make every FP8 linear's input
+ * and output-gradient, each also writing max|output| to *amax (nullable;
+ * zeroed by the call) so that moss_quant_mx2_fused runs with amax_given = 1
+ * (producer-fused amax).  Not reference functions:
+ * the reference's training harness is a 2-layer MLP (train.py:126-204); these
+ * implement the decoder the north_star trains.  All tensors row-major.
+ *
+ * RMSNorm over the last dim d (d % 8 == 0, d <= 8192), T rows:
+ *   x' = x + delta (bf16; written to x_out when delta != NULL)
+ *   y  = x' * rsqrt(mean(x'^2) + eps) * w   (f32 math, bf16 out), rstd[T] f32 */
+int moss_rmsnorm_fwd(const void* x, const void* delta, void* x_out, const float* w, float eps, void* y, float* rstd,
+                     float* amax, int64_t T, int64_t d, void* stream);
+/*   dx = rstd (dy w - xh mean(dy w xh)) + d_res   (xh = x' rstd; d_res nullable)
+ *   dw += sum_t dy xh  (f32, accumulated in a fixed order — deterministic;
+ *   dw nullable).  workspace: moss_rmsnorm_bwd_workspace_bytes(T, d) bytes. */
+int moss_rmsnorm_bwd(const void* dy, const void* x, const float* w, const float* rstd, const void* d_res, void* dx,
+                     float* dw, float* amax, float* workspace, int64_t T, int64_t d, void* stream);
+int64_t moss_rmsnorm_bwd_workspace_bytes(int64_t T, int64_t d);
+/* SwiGLU on gu = [gate | up] (T x 2f): h = silu(gate) * up (T x f) */
+int moss_swiglu_fwd(const void* gu, void* h, float* amax, int64_t T, int64_t f, void* stream);
+/* dgu = [dh up silu'(gate) | dh silu(gate)] */
+int moss_swiglu_bwd(const void* dh, const void* gu, void* dgu, float* amax, int64_t T, int64_t f, void* stream);
+/* RoPE: qkv [B, S, 3, H, hd] -> q, k, v [B, H, S, hd], q/k pairs (2i, 2i+1)
+ * rotated by cos/sin [S_max, hd/2] (f32) at position s */
+int moss_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q, void* k, void* v, int64_t B,
+                  int64_t S, int64_t H, int64_t hd, void* stream);
+/* dq, dk, dv [B, H, S, hd] -> dqkv [B, S, 3, H, hd] (inverse rotation) */
+int moss_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
+                  float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, void* stream);
+
 /* Human-readable status. */
 const char* moss_strerror(int status);
 

@@ -37,6 +37,13 @@ _SIGS = {
     "moss_quant_mx2": (_I, [_P, _I, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "moss_quant_mx2_fused": (_I, [_P, _I, _I64, _I64, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "moss_workspace_bytes": (_I64, []),
+    "moss_rmsnorm_fwd": (_I, [_P, _P, _P, _P, _F, _P, _P, _P, _I64, _I64, _P]),
+    "moss_rmsnorm_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _P]),
+    "moss_rmsnorm_bwd_workspace_bytes": (_I64, [_I64, _I64]),
+    "moss_swiglu_fwd": (_I, [_P, _P, _P, _I64, _I64, _P]),
+    "moss_swiglu_bwd": (_I, [_P, _P, _P, _P, _I64, _I64, _P]),
+    "moss_rope_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
+    "moss_rope_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
     "moss_encode_scaled": (_I, [_P, _I, _I64, _I64, _P, _F, _I, _P, _P, _P, _P, _P, _P]),
     "moss_gemm_mxf8": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _I, _P]),
     "moss_adamw_fp8": (_I, [_P, _P, _I, _P, _P, _I64, _I64, ctypes.POINTER(AdamParams), _F, _P, _P, _P,
@@ -267,3 +274,58 @@ def adamw_fp8(w, g, m, v, rows: int, cols: int, params: AdamParams, enc_scale: f
                                    cols, ctypes.byref(params), float(enc_scale), ptr(w_fp8), ptr(w_fp8_t),
                                    ptr(w_amax), ptr(n_saturated), flags.ptr, stream()),
               "moss_adamw_fp8")
+
+
+# ---------------------------------------------------------------- producer kernels (bf16)
+def _bf16(t, name):
+    if t is not None and t.dtype != torch.bfloat16:
+        raise errors.InvalidArgumentError(f"{name} must be bfloat16")
+
+
+def rmsnorm_fwd(x, delta, x_out, w, eps: float, y, rstd, amax) -> None:
+    T, d = x.shape
+    _bf16(x, "x"), _bf16(delta, "delta"), _bf16(y, "y")
+    with _Span("producer", T * d * (2 + 2 + (4 if delta is not None else 0))):
+        check(lib().moss_rmsnorm_fwd(x.data_ptr(), ptr(delta), ptr(x_out), w.data_ptr(), float(eps), y.data_ptr(),
+                                     rstd.data_ptr(), ptr(amax), T, d, stream()), "moss_rmsnorm_fwd")
+
+
+def rmsnorm_bwd(dy, x, w, rstd, d_res, dx, dw, amax) -> None:
+    """dw (nullable) is ACCUMULATED into (fixed-order reduction of per-CTA sums)."""
+    T, d = x.shape
+    _bf16(dy, "dy"), _bf16(x, "x"), _bf16(d_res, "d_res")
+    ws = None
+    if dw is not None:
+        nb = int(lib().moss_rmsnorm_bwd_workspace_bytes(T, d))
+        ws = torch.empty(max(nb, 4) // 4, dtype=torch.float32, device=x.device)
+    with _Span("producer", T * d * (2 + 2 + 2 + (2 if d_res is not None else 0)), kernels=2 if dw is not None else 1):
+        check(lib().moss_rmsnorm_bwd(dy.data_ptr(), x.data_ptr(), w.data_ptr(), rstd.data_ptr(), ptr(d_res),
+                                     dx.data_ptr(), ptr(dw), ptr(amax), ptr(ws), T, d, stream()), "moss_rmsnorm_bwd")
+
+
+def swiglu_fwd(gu, h, amax) -> None:
+    T, f2 = gu.shape
+    _bf16(gu, "gu")
+    with _Span("producer", T * f2 * 2 + T * f2):
+        check(lib().moss_swiglu_fwd(gu.data_ptr(), h.data_ptr(), ptr(amax), T, f2 // 2, stream()), "moss_swiglu_fwd")
+
+
+def swiglu_bwd(dh, gu, dgu, amax) -> None:
+    T, f2 = gu.shape
+    _bf16(dh, "dh"), _bf16(gu, "gu")
+    with _Span("producer", T * f2 * 2 * 2 + T * f2):
+        check(lib().moss_swiglu_bwd(dh.data_ptr(), gu.data_ptr(), dgu.data_ptr(), ptr(amax), T, f2 // 2, stream()),
+              "moss_swiglu_bwd")
+
+
+def rope_fwd(qkv, cos, sin, q, k, v, B: int, S: int, H: int, hd: int) -> None:
+    _bf16(qkv, "qkv")
+    with _Span("producer", B * S * 3 * H * hd * 4):
+        check(lib().moss_rope_fwd(qkv.data_ptr(), cos.data_ptr(), sin.data_ptr(), q.data_ptr(), k.data_ptr(),
+                                  v.data_ptr(), B, S, H, hd, stream()), "moss_rope_fwd")
+
+
+def rope_bwd(dq, dk, dv, cos, sin, dqkv, amax, B: int, S: int, H: int, hd: int) -> None:
+    with _Span("producer", B * S * 3 * H * hd * 4):
+        check(lib().moss_rope_bwd(dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), cos.data_ptr(), sin.data_ptr(),
+                                  dqkv.data_ptr(), ptr(amax), B, S, H, hd, stream()), "moss_rope_bwd")

@@ -23,6 +23,17 @@ int launch_adamw(float* w, const void* g, int g_dtype, float* m, float* v, int64
                  const moss_adam_params& p, float enc_scale, const moss_adam_params* p_dev, const float* enc_dev,
                  float* scale_out, uint8_t* w_fp8, uint8_t* w_fp8_t, float* w_amax, uint32_t* nsat,
                  uint32_t* flags, cudaStream_t st);
+int launch_rmsnorm_fwd(const void* x, const void* delta, void* x_out, const float* w, float eps, void* y, float* rstd,
+                       float* amax, int64_t T, int64_t d, cudaStream_t st);
+int launch_rmsnorm_bwd(const void* dy, const void* x, const float* w, const float* rstd, const void* d_res, void* dx,
+                       float* dw, float* amax, float* ws, int64_t T, int64_t d, cudaStream_t st);
+int64_t rmsnorm_bwd_workspace(int64_t T, int64_t d);
+int launch_swiglu_fwd(const void* gu, void* h, float* amax, int64_t T, int64_t f, cudaStream_t st);
+int launch_swiglu_bwd(const void* dh, const void* gu, void* dgu, float* amax, int64_t T, int64_t f, cudaStream_t st);
+int launch_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q, void* k, void* v, int64_t B,
+                    int64_t S, int64_t H, int64_t hd, cudaStream_t st);
+int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
+                    float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, cudaStream_t st);
 }  // namespace moss
 
 static inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
@@ -142,6 +153,61 @@ int moss_adamw_fp8_dev(float* w, const void* g, int g_dtype, float* m, float* v,
     moss_adam_params dummy{};
     return moss::launch_adamw(w, g, g_dtype, m, v, rows, cols, dummy, 1.0f, p_dev, enc_scale_dev, scale_out, w_fp8,
                               w_fp8_t, w_amax, n_saturated, flags, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------- producer kernels (bf16)
+static inline bool al16(const void* p) { return p == nullptr || aligned(p, 16); }
+
+int moss_rmsnorm_fwd(const void* x, const void* delta, void* x_out, const float* w, float eps, void* y, float* rstd,
+                     float* amax, int64_t T, int64_t d, void* stream) {
+    if (T <= 0 || d <= 0 || d % 8 || d > 8192 || T > INT32_MAX) return MOSS_ERR_SHAPE;
+    if (!x || !w || !y || !rstd || (delta && !x_out)) return MOSS_ERR_ARGUMENT;
+    if (!al16(x) || !al16(delta) || !al16(x_out) || !al16(w) || !al16(y)) return MOSS_ERR_ALIGN;
+    return moss::launch_rmsnorm_fwd(x, delta, x_out, w, eps, y, rstd, amax, T, d, (cudaStream_t)stream);
+}
+
+int64_t moss_rmsnorm_bwd_workspace_bytes(int64_t T, int64_t d) {
+    if (T <= 0 || d <= 0 || d % 8 || d > 8192) return -1;
+    return moss::rmsnorm_bwd_workspace(T, d);
+}
+
+int moss_rmsnorm_bwd(const void* dy, const void* x, const float* w, const float* rstd, const void* d_res, void* dx,
+                     float* dw, float* amax, float* workspace, int64_t T, int64_t d, void* stream) {
+    if (T <= 0 || d <= 0 || d % 8 || d > 8192 || T > INT32_MAX) return MOSS_ERR_SHAPE;
+    if (!dy || !x || !w || !rstd || !dx || (dw && !workspace)) return MOSS_ERR_ARGUMENT;
+    if (!al16(dy) || !al16(x) || !al16(w) || !al16(d_res) || !al16(dx) || !al16(dw) || !al16(workspace))
+        return MOSS_ERR_ALIGN;
+    return moss::launch_rmsnorm_bwd(dy, x, w, rstd, d_res, dx, dw, amax, workspace, T, d, (cudaStream_t)stream);
+}
+
+int moss_swiglu_fwd(const void* gu, void* h, float* amax, int64_t T, int64_t f, void* stream) {
+    if (T <= 0 || f <= 0 || f % 8) return MOSS_ERR_SHAPE;
+    if (!gu || !h) return MOSS_ERR_ARGUMENT;
+    if (!al16(gu) || !al16(h)) return MOSS_ERR_ALIGN;
+    return moss::launch_swiglu_fwd(gu, h, amax, T, f, (cudaStream_t)stream);
+}
+
+int moss_swiglu_bwd(const void* dh, const void* gu, void* dgu, float* amax, int64_t T, int64_t f, void* stream) {
+    if (T <= 0 || f <= 0 || f % 8) return MOSS_ERR_SHAPE;
+    if (!dh || !gu || !dgu) return MOSS_ERR_ARGUMENT;
+    if (!al16(dh) || !al16(gu) || !al16(dgu)) return MOSS_ERR_ALIGN;
+    return moss::launch_swiglu_bwd(dh, gu, dgu, amax, T, f, (cudaStream_t)stream);
+}
+
+int moss_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q, void* k, void* v, int64_t B,
+                  int64_t S, int64_t H, int64_t hd, void* stream) {
+    if (B <= 0 || S <= 0 || H <= 0 || hd <= 0 || hd % 8) return MOSS_ERR_SHAPE;
+    if (!qkv || !cosv || !sinv || !q || !k || !v) return MOSS_ERR_ARGUMENT;
+    if (!al16(qkv) || !al16(cosv) || !al16(sinv) || !al16(q) || !al16(k) || !al16(v)) return MOSS_ERR_ALIGN;
+    return moss::launch_rope_fwd(qkv, cosv, sinv, q, k, v, B, S, H, hd, (cudaStream_t)stream);
+}
+
+int moss_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
+                  float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, void* stream) {
+    if (B <= 0 || S <= 0 || H <= 0 || hd <= 0 || hd % 8) return MOSS_ERR_SHAPE;
+    if (!dq || !dk || !dv || !cosv || !sinv || !dqkv) return MOSS_ERR_ARGUMENT;
+    if (!al16(dq) || !al16(dk) || !al16(dv) || !al16(cosv) || !al16(sinv) || !al16(dqkv)) return MOSS_ERR_ALIGN;
+    return moss::launch_rope_bwd(dq, dk, dv, cosv, sinv, dqkv, amax, B, S, H, hd, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -1,0 +1,434 @@
+// Producer kernels of the MOSS activations and gradients (SURVEY.md 8(f)
+// rank 1: producer-fused amax).
+//
+// In the Llama decoder every FP8 linear's input and output-gradient is made
+// by one of these kernels: RMSNorm (forward: the qkv / gate_up inputs;
+// backward: the o / down output-gradients), SwiGLU (forward: the down input;
+// backward: the gate_up output-gradient) and RoPE (backward: the qkv
+// output-gradient).  Each kernel writes its bf16 output AND max|output| —
+// the tensor amax the two-level quantizer needs for g = amax/448
+// (quantize.py:149-155) — so the quantizer runs in its producer-amax mode:
+// one read of the tensor, no reduction pass, no grid barrier.
+//
+// The kernels are plain HBM-streaming elementwise / row-reduction kernels:
+// 16-byte vector loads/stores, f32 arithmetic, one pass.  amax is reduced
+// per CTA and merged with one atomicMax on the f32 bits (|y| >= 0 orders
+// like its bits; NaN/Inf land above 0x7F800000 and the quantizer flags them).
+// The caller zeroes the amax word (stream-ordered memset in the launcher).
+#include <algorithm>
+
+#include "common.cuh"
+#include "host_utils.cuh"
+
+namespace moss {
+
+__device__ __forceinline__ void bf16x8_load(const __nv_bfloat16* p, float (&v)[8]) { Vec8<__nv_bfloat16>::load(p, v); }
+
+__device__ __forceinline__ uint4 bf16x8_pack(const float (&v)[8]) {
+    uint4 o;
+    o.x = pack_bf16(v[0], v[1]);
+    o.y = pack_bf16(v[2], v[3]);
+    o.z = pack_bf16(v[4], v[5]);
+    o.w = pack_bf16(v[6], v[7]);
+    return o;
+}
+
+// |v| of the bf16-ROUNDED values (the tensor the quantizer will read)
+__device__ __forceinline__ uint32_t absmax_bits_bf16(const uint4& o) {
+    const uint32_t a = __vmaxu2(o.x & 0x7FFF7FFFu, o.y & 0x7FFF7FFFu);
+    const uint32_t b = __vmaxu2(o.z & 0x7FFF7FFFu, o.w & 0x7FFF7FFFu);
+    const uint32_t c = __vmaxu2(a, b);
+    return max(c & 0xFFFFu, c >> 16) << 16;   // as f32 bits
+}
+
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+    v += __shfl_xor_sync(0xFFFFFFFFu, v, 16);
+    v += __shfl_xor_sync(0xFFFFFFFFu, v, 8);
+    v += __shfl_xor_sync(0xFFFFFFFFu, v, 4);
+    v += __shfl_xor_sync(0xFFFFFFFFu, v, 2);
+    v += __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+    constexpr int NW = NT / 32;
+    if (NW == 1) return v;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();   // red reuse across calls
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) s += red[i];
+    return s;
+}
+
+__device__ __forceinline__ void block_amax_commit(uint32_t m, uint32_t* red_u, uint32_t* amax) {
+    if (!amax) return;
+    m = __reduce_max_sync(0xFFFFFFFFu, m);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red_u[warp] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t r = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r = max(r, red_u[i]);
+        if (r) atomicMax(amax, r);
+    }
+}
+
+// ------------------------------------------------------------------ RMSNorm
+// forward, one row per CTA iteration, NT threads x 8 elements (d = 8*NT):
+//   x' = x + delta (bf16, when delta != null; written to x_out)
+//   y  = bf16( f32(x') * rsqrt(mean(f32(x')^2) + eps) * w )
+//   rstd[t] = rsqrt(...), amax = max |y|
+template <int NT>
+__global__ void __launch_bounds__(NT) rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                         const __nv_bfloat16* __restrict__ delta,
+                                                         __nv_bfloat16* __restrict__ x_out, const float* __restrict__ w,
+                                                         float eps, __nv_bfloat16* __restrict__ y,
+                                                         float* __restrict__ rstd, uint32_t* amax, int T, int d) {
+    __shared__ float red[NT / 32];
+    __shared__ uint32_t red_u[NT / 32];
+    const int c = threadIdx.x * 8;
+    const bool act = c < d;
+    float wv[8];
+    if (act) {
+        const float4 a = *reinterpret_cast<const float4*>(w + c);
+        const float4 b = *reinterpret_cast<const float4*>(w + c + 4);
+        wv[0] = a.x; wv[1] = a.y; wv[2] = a.z; wv[3] = a.w; wv[4] = b.x; wv[5] = b.y; wv[6] = b.z; wv[7] = b.w;
+    }
+    uint32_t m = 0;
+    for (int t = blockIdx.x; t < T; t += gridDim.x) {
+        const int64_t off = (int64_t)t * d + c;
+        float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        float ss = 0.f;
+        if (act) {
+            bf16x8_load(x + off, v);
+            if (delta) {
+                float dv[8];
+                bf16x8_load(delta + off, dv);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i] + dv[i]));
+                *reinterpret_cast<uint4*>(x_out + off) = bf16x8_pack(v);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) ss = fmaf(v[i], v[i], ss);
+        }
+        ss = block_sum<NT>(ss, red);
+        const float r = rsqrtf(ss / (float)d + eps);
+        if (threadIdx.x == 0) rstd[t] = r;
+        if (act) {
+            float o[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] = v[i] * r * wv[i];
+            const uint4 ob = bf16x8_pack(o);
+            *reinterpret_cast<uint4*>(y + off) = ob;
+            m = max(m, absmax_bits_bf16(ob));
+        }
+    }
+    block_amax_commit(m, red_u, amax);
+}
+
+// backward: xh = f32(x') * rstd; gw = f32(dy) * w; c = mean(gw * xh)
+//   dx = bf16( rstd * (gw - xh * c) + f32(d_res) )   (d_res: gradient arriving
+//        through the residual stream; null = 0)
+//   dw += sum_t f32(dy) * xh   (per-CTA column sums, then a fixed-order
+//        reduction: deterministic, so replays and DP ranks agree bit for bit)
+//   amax = max |dx|
+template <int NT>
+__global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                         const __nv_bfloat16* __restrict__ x,
+                                                         const float* __restrict__ w, const float* __restrict__ rstd,
+                                                         const __nv_bfloat16* __restrict__ d_res,
+                                                         __nv_bfloat16* __restrict__ dx, float* __restrict__ dw_part,
+                                                         uint32_t* amax, int T, int d) {
+    __shared__ float red[NT / 32];
+    __shared__ uint32_t red_u[NT / 32];
+    const int c = threadIdx.x * 8;
+    const bool act = c < d;
+    float wv[8], dwp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (act) {
+        const float4 a = *reinterpret_cast<const float4*>(w + c);
+        const float4 b = *reinterpret_cast<const float4*>(w + c + 4);
+        wv[0] = a.x; wv[1] = a.y; wv[2] = a.z; wv[3] = a.w; wv[4] = b.x; wv[5] = b.y; wv[6] = b.z; wv[7] = b.w;
+    }
+    uint32_t m = 0;
+    const float inv_d = 1.0f / (float)d;
+    for (int t = blockIdx.x; t < T; t += gridDim.x) {
+        const int64_t off = (int64_t)t * d + c;
+        const float r = rstd[t];
+        float g[8], xh[8];
+        float dot = 0.f;
+        if (act) {
+            float dv[8];
+            bf16x8_load(dy + off, dv);
+            bf16x8_load(x + off, xh);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                xh[i] *= r;
+                g[i] = dv[i] * wv[i];
+                dot = fmaf(g[i], xh[i], dot);
+                dwp[i] = fmaf(dv[i], xh[i], dwp[i]);
+            }
+        }
+        dot = block_sum<NT>(dot, red) * inv_d;
+        if (act) {
+            float o[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] = r * (g[i] - xh[i] * dot);
+            if (d_res) {
+                float rv[8];
+                bf16x8_load(d_res + off, rv);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o[i] += rv[i];
+            }
+            const uint4 ob = bf16x8_pack(o);
+            *reinterpret_cast<uint4*>(dx + off) = ob;
+            m = max(m, absmax_bits_bf16(ob));
+        }
+    }
+    if (act && dw_part) {   // this CTA's column sums; reduced in a fixed order by rmsnorm_dw_reduce_kernel
+        float* dst = dw_part + (int64_t)blockIdx.x * d + c;
+        reinterpret_cast<float4*>(dst)[0] = make_float4(dwp[0], dwp[1], dwp[2], dwp[3]);
+        reinterpret_cast<float4*>(dst)[1] = make_float4(dwp[4], dwp[5], dwp[6], dwp[7]);
+    }
+    block_amax_commit(m, red_u, amax);
+}
+
+// dw[c] += sum_b part[b, c] in order b = 0, 1, ...
+__global__ void __launch_bounds__(256) rmsnorm_dw_reduce_kernel(const float* __restrict__ part, float* __restrict__ dw,
+                                                                int nb, int d) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= d) return;
+    float s = 0.f;
+    for (int b = 0; b < nb; ++b) s += part[(int64_t)b * d + c];
+    dw[c] += s;
+}
+
+// ------------------------------------------------------------------ SwiGLU
+// gu [T, 2f] = [gate | up];  h = bf16( silu(g) * u ),  amax = max |h|
+__global__ void __launch_bounds__(256) swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu,
+                                                         __nv_bfloat16* __restrict__ h, uint32_t* amax, int64_t T,
+                                                         int f) {
+    __shared__ uint32_t red_u[8];
+    const int64_t nv = T * (f / 8);
+    uint32_t m = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = i / (f / 8);
+        const int c = (int)(i - t * (f / 8)) * 8;
+        float g[8], u[8], o[8];
+        bf16x8_load(gu + t * 2 * f + c, g);
+        bf16x8_load(gu + t * 2 * f + f + c, u);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = g[k] / (1.0f + __expf(-g[k])) * u[k];
+        const uint4 ob = bf16x8_pack(o);
+        *reinterpret_cast<uint4*>(h + t * f + c) = ob;
+        m = max(m, absmax_bits_bf16(ob));
+    }
+    block_amax_commit(m, red_u, amax);
+}
+
+// dh [T, f] -> dgu [T, 2f]:  dg = dh * u * s * (1 + g (1 - s)),  du = dh * g * s,  s = sigmoid(g)
+__global__ void __launch_bounds__(256) swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dh,
+                                                         const __nv_bfloat16* __restrict__ gu,
+                                                         __nv_bfloat16* __restrict__ dgu, uint32_t* amax, int64_t T,
+                                                         int f) {
+    __shared__ uint32_t red_u[8];
+    const int64_t nv = T * (f / 8);
+    uint32_t m = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = i / (f / 8);
+        const int c = (int)(i - t * (f / 8)) * 8;
+        float g[8], u[8], d[8], og[8], ou[8];
+        bf16x8_load(gu + t * 2 * f + c, g);
+        bf16x8_load(gu + t * 2 * f + f + c, u);
+        bf16x8_load(dh + t * f + c, d);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float s = 1.0f / (1.0f + __expf(-g[k]));
+            og[k] = d[k] * u[k] * s * (1.0f + g[k] * (1.0f - s));
+            ou[k] = d[k] * g[k] * s;
+        }
+        const uint4 a = bf16x8_pack(og), b = bf16x8_pack(ou);
+        *reinterpret_cast<uint4*>(dgu + t * 2 * f + c) = a;
+        *reinterpret_cast<uint4*>(dgu + t * 2 * f + f + c) = b;
+        m = max(m, max(absmax_bits_bf16(a), absmax_bits_bf16(b)));
+    }
+    block_amax_commit(m, red_u, amax);
+}
+
+// ------------------------------------------------------------------ RoPE
+// qkv [B, S, 3, H, hd] (the qkv projection output) -> q, k, v [B, H, S, hd]
+// with q, k rotated by (cos, sin)[s, i] on the pairs (2i, 2i+1):
+//   (a, b) -> (a c - b s, a s + b c)
+__global__ void __launch_bounds__(256) rope_fwd_kernel(const __nv_bfloat16* __restrict__ qkv,
+                                                       const float* __restrict__ cosv, const float* __restrict__ sinv,
+                                                       __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ k,
+                                                       __nv_bfloat16* __restrict__ v, int B, int S, int H, int hd) {
+    const int vh = hd / 8;   // 8-element vectors per head
+    const int64_t nv = (int64_t)B * S * H * vh;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(i % vh);
+        const int64_t r = i / vh;
+        const int h = (int)(r % H);
+        const int64_t bs = r / H;
+        const int s = (int)(bs % S);
+        const int b = (int)(bs / S);
+        const int64_t src = bs * 3 * H * hd + (int64_t)h * hd + j * 8;
+        const int64_t dst = (((int64_t)b * H + h) * S + s) * hd + j * 8;
+        const float* cs = cosv + (int64_t)s * (hd / 2) + j * 4;
+        const float* sn = sinv + (int64_t)s * (hd / 2) + j * 4;
+        float qa[8], ka[8], qo[8], ko[8];
+        bf16x8_load(qkv + src, qa);
+        bf16x8_load(qkv + src + (int64_t)H * hd, ka);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const float c = cs[p], sv = sn[p];
+            qo[2 * p] = qa[2 * p] * c - qa[2 * p + 1] * sv;
+            qo[2 * p + 1] = qa[2 * p] * sv + qa[2 * p + 1] * c;
+            ko[2 * p] = ka[2 * p] * c - ka[2 * p + 1] * sv;
+            ko[2 * p + 1] = ka[2 * p] * sv + ka[2 * p + 1] * c;
+        }
+        *reinterpret_cast<uint4*>(q + dst) = bf16x8_pack(qo);
+        *reinterpret_cast<uint4*>(k + dst) = bf16x8_pack(ko);
+        *reinterpret_cast<uint4*>(v + dst) = *reinterpret_cast<const uint4*>(qkv + src + 2 * (int64_t)H * hd);
+    }
+}
+
+// dq, dk, dv [B, H, S, hd] -> dqkv [B, S, 3, H, hd] (inverse rotation), amax = max |dqkv|
+__global__ void __launch_bounds__(256) rope_bwd_kernel(const __nv_bfloat16* __restrict__ dq,
+                                                       const __nv_bfloat16* __restrict__ dk,
+                                                       const __nv_bfloat16* __restrict__ dv,
+                                                       const float* __restrict__ cosv, const float* __restrict__ sinv,
+                                                       __nv_bfloat16* __restrict__ dqkv, uint32_t* amax, int B, int S,
+                                                       int H, int hd) {
+    __shared__ uint32_t red_u[8];
+    const int vh = hd / 8;
+    const int64_t nv = (int64_t)B * S * H * vh;
+    uint32_t m = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(i % vh);
+        const int64_t r = i / vh;
+        const int h = (int)(r % H);
+        const int64_t bs = r / H;
+        const int s = (int)(bs % S);
+        const int b = (int)(bs / S);
+        const int64_t dst = bs * 3 * H * hd + (int64_t)h * hd + j * 8;
+        const int64_t src = (((int64_t)b * H + h) * S + s) * hd + j * 8;
+        const float* cs = cosv + (int64_t)s * (hd / 2) + j * 4;
+        const float* sn = sinv + (int64_t)s * (hd / 2) + j * 4;
+        float qa[8], ka[8], qo[8], ko[8];
+        bf16x8_load(dq + src, qa);
+        bf16x8_load(dk + src, ka);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const float c = cs[p], sv = sn[p];
+            qo[2 * p] = qa[2 * p] * c + qa[2 * p + 1] * sv;
+            qo[2 * p + 1] = -qa[2 * p] * sv + qa[2 * p + 1] * c;
+            ko[2 * p] = ka[2 * p] * c + ka[2 * p + 1] * sv;
+            ko[2 * p + 1] = -ka[2 * p] * sv + ka[2 * p + 1] * c;
+        }
+        const uint4 a = bf16x8_pack(qo), bb = bf16x8_pack(ko);
+        const uint4 vv = *reinterpret_cast<const uint4*>(dv + src);
+        *reinterpret_cast<uint4*>(dqkv + dst) = a;
+        *reinterpret_cast<uint4*>(dqkv + dst + (int64_t)H * hd) = bb;
+        *reinterpret_cast<uint4*>(dqkv + dst + 2 * (int64_t)H * hd) = vv;
+        m = max(m, max(absmax_bits_bf16(a), max(absmax_bits_bf16(bb), absmax_bits_bf16(vv))));
+    }
+    block_amax_commit(m, red_u, amax);
+}
+
+// ------------------------------------------------------------------ launchers
+static int grid_for(int64_t work, int threads, int per_sm) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((work + threads - 1) / threads, (int64_t)sm_count() * per_sm));
+}
+
+static int amax_reset(uint32_t* amax, cudaStream_t st) {
+    return (amax && cudaMemsetAsync(amax, 0, 4, st) != cudaSuccess) ? MOSS_ERR_CUDA : MOSS_OK;
+}
+
+int launch_rmsnorm_fwd(const void* x, const void* delta, void* x_out, const float* w, float eps, void* y, float* rstd,
+                       float* amax, int64_t T, int64_t d, cudaStream_t st) {
+    if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
+    const int nt = (int)((d / 8 + 31) / 32 * 32);
+    const int grid = (int)std::min<int64_t>(T, (int64_t)sm_count() * (2048 / nt));
+    auto args = [&](auto kern) {
+        kern<<<grid, nt, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)delta,
+                                                  (__nv_bfloat16*)x_out, w, eps, (__nv_bfloat16*)y, rstd,
+                                                  reinterpret_cast<uint32_t*>(amax), (int)T, (int)d);
+    };
+    switch (nt) {
+        case 32: args(rmsnorm_fwd_kernel<32>); break;
+        case 64: args(rmsnorm_fwd_kernel<64>); break;
+        case 96: args(rmsnorm_fwd_kernel<96>); break;
+        case 128: args(rmsnorm_fwd_kernel<128>); break;
+        case 256: args(rmsnorm_fwd_kernel<256>); break;
+        case 512: args(rmsnorm_fwd_kernel<512>); break;
+        case 1024: args(rmsnorm_fwd_kernel<1024>); break;
+        default: return MOSS_ERR_SHAPE;
+    }
+    return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+}
+
+static int rmsnorm_bwd_grid(int64_t T, int64_t d) {
+    const int nt = (int)((d / 8 + 31) / 32 * 32);
+    return (int)std::min<int64_t>(T, (int64_t)sm_count() * std::max(1, 1024 / nt));
+}
+
+int64_t rmsnorm_bwd_workspace(int64_t T, int64_t d) { return (int64_t)rmsnorm_bwd_grid(T, d) * d * 4; }
+
+int launch_rmsnorm_bwd(const void* dy, const void* x, const float* w, const float* rstd, const void* d_res, void* dx,
+                       float* dw, float* amax, float* ws, int64_t T, int64_t d, cudaStream_t st) {
+    if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
+    const int nt = (int)((d / 8 + 31) / 32 * 32);
+    const int grid = rmsnorm_bwd_grid(T, d);
+    auto args = [&](auto kern) {
+        kern<<<grid, nt, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, w, rstd,
+                                  (const __nv_bfloat16*)d_res, (__nv_bfloat16*)dx, dw ? ws : nullptr,
+                                  reinterpret_cast<uint32_t*>(amax), (int)T, (int)d);
+    };
+    switch (nt) {
+        case 32: args(rmsnorm_bwd_kernel<32>); break;
+        case 64: args(rmsnorm_bwd_kernel<64>); break;
+        case 96: args(rmsnorm_bwd_kernel<96>); break;
+        case 128: args(rmsnorm_bwd_kernel<128>); break;
+        case 256: args(rmsnorm_bwd_kernel<256>); break;
+        case 512: args(rmsnorm_bwd_kernel<512>); break;
+        case 1024: args(rmsnorm_bwd_kernel<1024>); break;
+        default: return MOSS_ERR_SHAPE;
+    }
+    if (dw) rmsnorm_dw_reduce_kernel<<<(unsigned)((d + 255) / 256), 256, 0, st>>>(ws, dw, grid, (int)d);
+    return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+}
+
+int launch_swiglu_fwd(const void* gu, void* h, float* amax, int64_t T, int64_t f, cudaStream_t st) {
+    if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
+    swiglu_fwd_kernel<<<grid_for(T * (f / 8), 256, 8), 256, 0, st>>>(
+        (const __nv_bfloat16*)gu, (__nv_bfloat16*)h, reinterpret_cast<uint32_t*>(amax), T, (int)f);
+    return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+}
+
+int launch_swiglu_bwd(const void* dh, const void* gu, void* dgu, float* amax, int64_t T, int64_t f, cudaStream_t st) {
+    if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
+    swiglu_bwd_kernel<<<grid_for(T * (f / 8), 256, 8), 256, 0, st>>>(
+        (const __nv_bfloat16*)dh, (const __nv_bfloat16*)gu, (__nv_bfloat16*)dgu, reinterpret_cast<uint32_t*>(amax), T,
+        (int)f);
+    return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+}
+
+int launch_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q, void* k, void* v, int64_t B,
+                    int64_t S, int64_t H, int64_t hd, cudaStream_t st) {
+    rope_fwd_kernel<<<grid_for(B * S * H * (hd / 8), 256, 8), 256, 0, st>>>(
+        (const __nv_bfloat16*)qkv, cosv, sinv, (__nv_bfloat16*)q, (__nv_bfloat16*)k, (__nv_bfloat16*)v, (int)B, (int)S,
+        (int)H, (int)hd);
+    return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+}
+
+int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
+                    float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, cudaStream_t st) {
+    if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
+    rope_bwd_kernel<<<grid_for(B * S * H * (hd / 8), 256, 8), 256, 0, st>>>(
+        (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv, cosv, sinv,
+        (__nv_bfloat16*)dqkv, reinterpret_cast<uint32_t*>(amax), (int)B, (int)S, (int)H, (int)hd);
+    return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+}
+
+}  // namespace moss

@@ -23,6 +23,7 @@ import torch.nn.functional as F
 from torch import nn
 
 from .nn import MossLinear
+from .producers import AddRMSNormFn, RMSNormFn, RopeQKVFn, SwiGLUFn
 
 __all__ = ["LlamaConfig", "LlamaModel", "MarkovTokens", "LLAMA_125M", "LLAMA2_7B"]
 
@@ -42,6 +43,7 @@ class LlamaConfig:
     interval: int = 500
     compute_dtype: torch.dtype = torch.bfloat16
     fp8_backward: bool = True       # False: reference semantics, full-precision backward (train.py:187-192)
+    fused_ops: bool = True          # sm_100a producer kernels (RMSNorm/SwiGLU/RoPE + amax); False: torch glue
 
     @property
     def head_dim(self) -> int:
@@ -122,8 +124,17 @@ class Block(nn.Module):
         self.mlp_norm = RMSNorm(d, cfg.norm_eps, device)
         self.gate_up = _linear(cfg, d, 2 * f, device)
         self.down = _linear(cfg, f, d, device)
+        self.fused = cfg.fused_ops and all(isinstance(m, MossLinear) for m in (self.qkv, self.o, self.gate_up, self.down))
 
-    def forward(self, x, cos, sin):
+    def forward(self, x, cos, sin, delta=None, prev=None):
+        """Returns the block output.  Fused path (``cfg.fused_ops`` with MOSS
+        linears): takes and returns the residual stream lazily as (x, delta)
+        with x + delta folded into the next RMSNorm kernel; ``prev`` is the
+        MossLinear that produced delta (its dY comes out of that kernel)."""
+        if self.fused:
+            return self._forward_fused(x, cos, sin, delta, prev)
+        if delta is not None:
+            x = x + delta
         B, S, d = x.shape
         H, hd = self.cfg.n_heads, self.cfg.head_dim
         q, k, v = self.qkv(self.attn_norm(x)).split(d, dim=-1)
@@ -133,7 +144,22 @@ class Block(nn.Module):
         a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
         x = x + self.o(a.transpose(1, 2).reshape(B, S, d))
         g, u = self.gate_up(self.mlp_norm(x)).split(self.cfg.d_ffn, dim=-1)
-        return x + self.down(F.silu(g) * u)
+        return x + self.down(F.silu(g) * u), None
+
+    def _forward_fused(self, x, cos, sin, delta, prev):
+        B, S, d = x.shape
+        H = self.cfg.n_heads
+        eps = self.cfg.norm_eps
+        if delta is None:
+            y, am = RMSNormFn.apply(x, self.attn_norm.weight, eps, prev)
+        else:
+            x, y, am = AddRMSNormFn.apply(x, delta, self.attn_norm.weight, eps, prev)
+        q, k, v = RopeQKVFn.apply(self.qkv(y, am), cos, sin, H, self.qkv)
+        a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+        o = self.o(a.transpose(1, 2).reshape(B, S, d))
+        x, y, am = AddRMSNormFn.apply(x, o, self.mlp_norm.weight, eps, self.o)
+        h, am = SwiGLUFn.apply(self.gate_up(y, am), self.gate_up)
+        return x, self.down(h, am)
 
 
 class LlamaModel(nn.Module):
@@ -150,9 +176,14 @@ class LlamaModel(nn.Module):
 
     def forward(self, tokens: torch.Tensor, targets: torch.Tensor | None = None):
         x = F.embedding(tokens, self.embed).to(self.cfg.compute_dtype)
+        delta, prev = None, None
         for blk in self.blocks:
-            x = blk(x, self.cos, self.sin)
-        x = self.norm(x)
+            x, delta = blk(x, self.cos, self.sin, delta, prev)
+            prev = blk.down
+        if delta is not None:
+            _, x, _ = AddRMSNormFn.apply(x, delta, self.norm.weight, self.cfg.norm_eps, prev)
+        else:
+            x = self.norm(x)
         logits = F.linear(x, self.head.to(self.cfg.compute_dtype))
         if targets is None:
             return logits

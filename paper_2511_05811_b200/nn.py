@@ -75,15 +75,20 @@ class MossLinearFunction(torch.autograd.Function):
     # the dependency; its gradient is returned as None and instead written by
     # the wgrad GEMM straight into ``weight.main_grad`` (FP32, possibly a DP
     # bucket view), with no extra pass over the gradient.
+    # ``amax`` (optional, device f32 [1]) is max|x| computed by the kernel that
+    # produced x (producer-fused amax): the quantizer then skips its reduction.
     @staticmethod
-    def forward(ctx, x: torch.Tensor, weight: torch.Tensor, layer: "MossLinear") -> torch.Tensor:
+    def forward(ctx, x: torch.Tensor, weight: torch.Tensor, layer: "MossLinear",
+                amax: torch.Tensor | None = None) -> torch.Tensor:
         k = x.shape[-1]
         n = layer.out_features
         x2d = _aligned_2d(x, k)
+        if x2d.data_ptr() != x.data_ptr() or x2d.dtype != x.dtype:
+            amax = None                                 # the quantized tensor is not the producer's
         need_w = weight.requires_grad
         flags = device_flags(x.device)
         fp8_bwd = layer.fp8_backward
-        op = quantize_mx2(x2d, row=True, col=need_w and fp8_bwd, flags=flags)
+        op = quantize_mx2(x2d, row=True, col=need_w and fp8_bwd, flags=flags, amax=amax)
         y = mx_gemm(op.codes, op.sf, op.g, layer.w_fp8, None, layer.w_scale, out_dtype=torch.bfloat16)
         ctx.layer = layer
         ctx.fp8_bwd = fp8_bwd
@@ -107,7 +112,7 @@ class MossLinearFunction(torch.autograd.Function):
             return MossLinearFunction._backward_fp(ctx, dy, layer, need_x)
         dy2d = _aligned_2d(dy, n)
         flags = device_flags(dy.device)
-        opd = quantize_mx2(dy2d, row=need_x, col=ctx.need_w, flags=flags)
+        opd = quantize_mx2(dy2d, row=need_x, col=ctx.need_w, flags=flags, amax=layer.take_dy_amax(dy2d))
         dx = None
         if need_x:
             dx = mx_gemm(opd.codes, opd.sf, opd.g, layer.w_fp8_t, None, layer.w_scale, out_dtype=torch.bfloat16)
@@ -127,7 +132,7 @@ class MossLinearFunction(torch.autograd.Function):
             hook = getattr(w, "grad_ready_hook", None)
             if hook is not None:
                 hook(w)
-        return dx, None, None
+        return dx, None, None, None
 
     @staticmethod
     def _backward_fp(ctx, dy, layer, need_x):
@@ -149,7 +154,8 @@ class MossLinearFunction(torch.autograd.Function):
             hook = getattr(w, "grad_ready_hook", None)
             if hook is not None:
                 hook(w)
-        return dx, None, None
+        layer.take_dy_amax(dy2d)
+        return dx, None, None, None
 
 
 class MossLinear(nn.Module):
@@ -183,6 +189,26 @@ class MossLinear(nn.Module):
         self.register_buffer("w_amax", torch.zeros(1, dtype=torch.float32, device=device), persistent=False)
         self.interval = interval
         self.schedule: ScaleSchedule | None = None
+        # producer-fused amax of this layer's output-gradient (set by the
+        # backward of the op that consumes our output, read by our backward)
+        self.register_buffer("dy_amax", torch.zeros(1, dtype=torch.float32, device=device), persistent=False)
+        self._dy_amax_ptr = None
+
+    def offer_dy_amax(self, dy: torch.Tensor) -> torch.Tensor:
+        """Called by the producer of dY before it launches: returns the amax
+        buffer to fill and remembers which tensor it describes."""
+        self._dy_amax_ptr = (dy.data_ptr(), tuple(dy.shape))
+        return self.dy_amax
+
+    def take_dy_amax(self, dy2d: torch.Tensor) -> torch.Tensor | None:
+        """The producer's amax if it describes exactly ``dy2d`` (else None)."""
+        want, self._dy_amax_ptr = self._dy_amax_ptr, None
+        if want is None or want[0] != dy2d.data_ptr() or dy2d.dtype != torch.bfloat16:
+            return None
+        n = 1
+        for s in want[1]:
+            n *= s
+        return self.dy_amax if n == dy2d.numel() else None
 
     @torch.no_grad()
     def init_fp8(self) -> None:
@@ -203,10 +229,10 @@ class MossLinear(nn.Module):
         _lib.encode_scaled(self.weight.detach(), device_flags(self.weight.device), scale_host=s,
                            codes=self.w_fp8, codes_t=self.w_fp8_t if self.out_features % 32 == 0 else None)
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, amax: torch.Tensor | None = None) -> torch.Tensor:
         if self.schedule is None:
             self.init_fp8()
-        return MossLinearFunction.apply(x, self.weight, self)
+        return MossLinearFunction.apply(x, self.weight, self, amax)
 
     def extra_repr(self) -> str:
         return f"in_features={self.in_features}, out_features={self.out_features}, fp8=e4m3(mx2 act, per-tensor W)"

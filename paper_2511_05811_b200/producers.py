@@ -1,0 +1,144 @@
+"""Autograd wrappers of the producer kernels (csrc/producers.cu): the Llama
+ops that make each FP8 linear's input and output-gradient, with the tensor
+amax computed in the same pass (producer-fused amax).
+
+Forward: RMSNorm -> (y, amax) feeds MossLinear(y, amax=...) of qkv / gate_up;
+SwiGLU -> (h, amax) feeds the down projection.  Backward: each op writes
+amax(dX) into the buffer of the MossLinear whose output-gradient dX is
+(``consumer.offer_dy_amax``), so that layer's two-level quantizer runs in
+producer-amax mode: one read of dY, no reduction pass.
+
+The residual add is folded into the next RMSNorm (``AddRMSNormFn``):
+x' = x + delta and y = norm(x') in one kernel; its backward adds the
+residual-stream gradient into dx in the same kernel.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+__all__ = ["RMSNormFn", "AddRMSNormFn", "SwiGLUFn", "RopeQKVFn"]
+
+
+def _c2(t: torch.Tensor, d: int) -> torch.Tensor:
+    t2 = t.reshape(-1, d)
+    return t2 if t2.is_contiguous() else t2.contiguous()
+
+
+def _amax_buf(consumer, out: torch.Tensor) -> torch.Tensor | None:
+    return consumer.offer_dy_amax(out) if consumer is not None else None
+
+
+class RMSNormFn(torch.autograd.Function):
+    """y = norm(x) * w; returns (y, amax(y)).  ``consumer``: the MossLinear whose
+    dY is dx (None when x's producer does not quantize its gradient)."""
+
+    @staticmethod
+    def forward(ctx, x, weight, eps: float, consumer):
+        d = x.shape[-1]
+        x2 = _c2(x, d)
+        T = x2.shape[0]
+        y = torch.empty_like(x2)
+        rstd = torch.empty(T, dtype=torch.float32, device=x.device)
+        amax = torch.empty(1, dtype=torch.float32, device=x.device)
+        _lib.rmsnorm_fwd(x2, None, None, weight, eps, y, rstd, amax)
+        ctx.save_for_backward(x2, weight, rstd)
+        ctx.consumer, ctx.shape = consumer, x.shape
+        ctx.mark_non_differentiable(amax)
+        return y.view(x.shape), amax
+
+    @staticmethod
+    def backward(ctx, dy, _damax):
+        x2, weight, rstd = ctx.saved_tensors
+        d = x2.shape[1]
+        dx = torch.empty_like(x2)
+        dw = torch.zeros_like(weight)
+        _lib.rmsnorm_bwd(_c2(dy, d), x2, weight, rstd, None, dx, dw, _amax_buf(ctx.consumer, dx))
+        return dx.view(ctx.shape), dw, None, None
+
+
+class AddRMSNormFn(torch.autograd.Function):
+    """x' = x + delta; y = norm(x') * w; returns (x', y, amax(y)).
+    Backward: dx' (residual stream) + norm'(dy) -> the gradient of both x and
+    delta; ``consumer`` is the MossLinear that produced delta (its dY)."""
+
+    @staticmethod
+    def forward(ctx, x, delta, weight, eps: float, consumer):
+        d = x.shape[-1]
+        x2, d2 = _c2(x, d), _c2(delta, d)
+        T = x2.shape[0]
+        xn = torch.empty_like(x2)
+        y = torch.empty_like(x2)
+        rstd = torch.empty(T, dtype=torch.float32, device=x.device)
+        amax = torch.empty(1, dtype=torch.float32, device=x.device)
+        _lib.rmsnorm_fwd(x2, d2, xn, weight, eps, y, rstd, amax)
+        ctx.save_for_backward(xn, weight, rstd)
+        ctx.consumer, ctx.shape = consumer, x.shape
+        ctx.mark_non_differentiable(amax)
+        return xn.view(x.shape), y.view(x.shape), amax
+
+    @staticmethod
+    def backward(ctx, dxn, dy, _damax):
+        xn, weight, rstd = ctx.saved_tensors
+        d = xn.shape[1]
+        dx = torch.empty_like(xn)
+        dw = torch.zeros_like(weight)
+        if dy is None:
+            dy = torch.zeros_like(xn)
+        _lib.rmsnorm_bwd(_c2(dy, d), xn, weight, rstd, None if dxn is None else _c2(dxn, d), dx, dw,
+                         _amax_buf(ctx.consumer, dx))
+        g = dx.view(ctx.shape)
+        return g, g, dw, None, None
+
+
+class SwiGLUFn(torch.autograd.Function):
+    """gu = [gate | up] -> (h = silu(gate) * up, amax(h)); ``consumer`` is the
+    gate_up MossLinear (its dY is dgu)."""
+
+    @staticmethod
+    def forward(ctx, gu, consumer):
+        f2 = gu.shape[-1]
+        gu2 = _c2(gu, f2)
+        h = torch.empty(gu2.shape[0], f2 // 2, dtype=gu.dtype, device=gu.device)
+        amax = torch.empty(1, dtype=torch.float32, device=gu.device)
+        _lib.swiglu_fwd(gu2, h, amax)
+        ctx.save_for_backward(gu2)
+        ctx.consumer, ctx.shape = consumer, gu.shape
+        ctx.mark_non_differentiable(amax)
+        return h.view(*gu.shape[:-1], f2 // 2), amax
+
+    @staticmethod
+    def backward(ctx, dh, _damax):
+        (gu2,) = ctx.saved_tensors
+        dgu = torch.empty_like(gu2)
+        _lib.swiglu_bwd(_c2(dh, gu2.shape[1] // 2), gu2, dgu, _amax_buf(ctx.consumer, dgu))
+        return dgu.view(ctx.shape), None
+
+
+class RopeQKVFn(torch.autograd.Function):
+    """qkv [B, S, 3*H*hd] -> q, k, v [B, H, S, hd] (q, k rotated).  Backward
+    assembles dqkv with the inverse rotation; ``consumer`` is the qkv layer."""
+
+    @staticmethod
+    def forward(ctx, qkv, cos, sin, n_heads: int, consumer):
+        B, S, three_d = qkv.shape
+        hd = three_d // (3 * n_heads)
+        qkv = qkv if qkv.is_contiguous() else qkv.contiguous()
+        q = torch.empty(B, n_heads, S, hd, dtype=qkv.dtype, device=qkv.device)
+        k, v = torch.empty_like(q), torch.empty_like(q)
+        _lib.rope_fwd(qkv, cos, sin, q, k, v, B, S, n_heads, hd)
+        ctx.save_for_backward(cos, sin)
+        ctx.dims, ctx.consumer = (B, S, n_heads, hd), consumer
+        return q, k, v
+
+    @staticmethod
+    def backward(ctx, dq, dk, dv):
+        cos, sin = ctx.saved_tensors
+        B, S, H, hd = ctx.dims
+        dq, dk, dv = (t.contiguous() if t is not None else torch.zeros(B, H, S, hd, dtype=torch.bfloat16,
+                                                                        device=cos.device) for t in (dq, dk, dv))
+        dqkv = torch.empty(B, S, 3 * H * hd, dtype=dq.dtype, device=dq.device)
+        _lib.rope_bwd(dq, dk, dv, cos, sin, dqkv, _amax_buf(ctx.consumer, dqkv.view(B * S, -1)), B, S, H, hd)
+        return dqkv, None, None, None, None

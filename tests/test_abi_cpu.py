@@ -54,6 +54,23 @@ def test_argument_checks_precede_launch():
     assert lib.moss_amax(odd, 1, 64, fake, fake, None) == 6
     # bad dtype
     assert lib.moss_amax(fake, 7, 64, fake, fake, None) == 3
+    # fused quantizer: workspace is required; cols % 32
+    assert lib.moss_quant_mx2_fused(fake, 1, 128, 128, fake, 0, fake, fake, None, None, None, None, fake, None,
+                                    fake, None) == 3
+    assert lib.moss_quant_mx2_fused(fake, 1, 128, 100, fake, 0, fake, fake, None, None, None, None, fake, fake,
+                                    fake, None) == 1
+    assert lib.moss_workspace_bytes() >= 16
+    # producer kernels: d % 8, d <= 8192, f % 8, hd % 8, missing outputs
+    assert lib.moss_rmsnorm_fwd(fake, None, None, fake, ctypes.c_float(1e-5), fake, fake, None, 4, 100, None) == 1
+    assert lib.moss_rmsnorm_fwd(fake, None, None, fake, ctypes.c_float(1e-5), fake, fake, None, 4, 16384, None) == 1
+    assert lib.moss_rmsnorm_fwd(fake, fake, None, fake, ctypes.c_float(1e-5), fake, fake, None, 4, 128, None) == 3
+    assert lib.moss_rmsnorm_bwd(fake, fake, fake, fake, None, None, None, None, None, 4, 128, None) == 3
+    assert lib.moss_rmsnorm_bwd(fake, fake, fake, fake, None, fake, fake, None, None, 4, 128, None) == 3  # dw w/o ws
+    assert lib.moss_rmsnorm_bwd_workspace_bytes(4, 100) == -1
+    assert lib.moss_swiglu_fwd(fake, fake, None, 4, 12, None) == 1
+    assert lib.moss_swiglu_bwd(odd, fake, fake, None, 4, 16, None) == 6
+    assert lib.moss_rope_fwd(fake, fake, fake, fake, fake, fake, 1, 4, 2, 12, None) == 1
+    assert lib.moss_rope_bwd(fake, fake, fake, fake, fake, None, None, 1, 4, 2, 16, None) == 3
     with pytest.raises(errors.InvalidShapeError):
         _lib.check(1, "x")
     with pytest.raises(errors.E8m0RangeError):

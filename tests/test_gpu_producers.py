@@ -1,0 +1,164 @@
+"""Producer kernels (csrc/producers.cu) vs plain PyTorch fp32 references of
+the same ops, and the fused Llama block vs the torch-glue block.
+
+Tolerances: outputs are bf16, so the gate is bf16 rounding of the fp32
+reference (|err| <= 2^-7 |ref| + small abs).  The amax the kernels emit must
+equal max|output| of the bf16 tensor they wrote, exactly (it becomes the
+quantizer's global scale, quantize.py:149-155)."""
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import torch.nn.functional as F  # noqa: E402
+
+from paper_2511_05811_b200 import _lib  # noqa: E402
+from paper_2511_05811_b200 import llama as L  # noqa: E402
+from paper_2511_05811_b200 import nn as mnn  # noqa: E402
+from paper_2511_05811_b200.producers import AddRMSNormFn, RMSNormFn, RopeQKVFn, SwiGLUFn  # noqa: E402
+
+
+def close_bf16(got, ref, rtol=2 ** -7, atol=1e-5):
+    err = (got.float() - ref.float()).abs()
+    bound = rtol * ref.float().abs() + atol
+    assert bool((err <= bound).all()), f"max excess {float((err - bound).max())}"
+
+
+def exact_amax(amax, t):
+    assert float(amax) == float(t.detach().float().abs().max())
+
+
+def test_rmsnorm_dw_deterministic():
+    torch.manual_seed(3)
+    T, d = 4096, 4096
+    x = torch.randn(T, d, device="cuda", dtype=torch.bfloat16)
+    w = torch.randn(d, device="cuda")
+    rstd = torch.rand(T, device="cuda") + 0.5
+    dy = torch.randn(T, d, device="cuda", dtype=torch.bfloat16)
+    outs = []
+    for _ in range(3):
+        dx = torch.empty_like(x)
+        dw = torch.zeros(d, device="cuda")
+        _lib.rmsnorm_bwd(dy, x, w, rstd, None, dx, dw, None)
+        outs.append((dx, dw))
+    for dx, dw in outs[1:]:
+        assert torch.equal(dx, outs[0][0]) and torch.equal(dw, outs[0][1])
+
+
+@pytest.mark.parametrize("T,d", [(64, 128), (256, 768), (512, 4096)])
+@pytest.mark.parametrize("residual", [False, True])
+def test_rmsnorm_fwd_bwd(T, d, residual):
+    torch.manual_seed(T + d)
+    x = torch.randn(T, d, device="cuda", dtype=torch.bfloat16)
+    delta = torch.randn(T, d, device="cuda", dtype=torch.bfloat16) if residual else None
+    w = (1 + 0.1 * torch.randn(d, device="cuda")).requires_grad_(True)
+    eps = 1e-5
+    xin = x.clone().requires_grad_(True)
+    din = delta.clone().requires_grad_(True) if residual else None
+    if residual:
+        xn, y, am = AddRMSNormFn.apply(xin, din, w, eps, None)
+    else:
+        y, am = RMSNormFn.apply(xin, w, eps, None)
+    # fp32 reference on the same bf16 residual sum
+    xr = (x + delta) if residual else x
+    if residual:
+        assert torch.equal(xn, xr)
+    xf = xr.float().requires_grad_(True)
+    wf = w.detach().clone().requires_grad_(True)
+    yf = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps) * wf
+    close_bf16(y, yf)
+    exact_amax(am, y)
+    dy = torch.randn(T, d, device="cuda", dtype=torch.bfloat16)
+    dres = torch.randn(T, d, device="cuda", dtype=torch.bfloat16) if residual else None
+    if residual:
+        torch.autograd.backward([xn, y], [dres, dy])
+    else:
+        y.backward(dy)
+    yf.backward(dy.float())
+    gx_ref = xf.grad + (dres.float() if residual else 0)
+    close_bf16(xin.grad, gx_ref, rtol=2 ** -6, atol=1e-3)
+    if residual:
+        assert torch.equal(din.grad, xin.grad)
+    assert torch.allclose(w.grad, wf.grad, rtol=1e-3, atol=1e-2)
+
+
+@pytest.mark.parametrize("T,f", [(64, 256), (1024, 2048), (512, 11008)])
+def test_swiglu_fwd_bwd(T, f):
+    torch.manual_seed(f)
+    gu = (torch.randn(T, 2 * f, device="cuda") * 2).to(torch.bfloat16).requires_grad_(True)
+    h, am = SwiGLUFn.apply(gu, None)
+    gf = gu.detach().float().requires_grad_(True)
+    hf = F.silu(gf[:, :f]) * gf[:, f:]
+    close_bf16(h, hf, atol=1e-4)
+    exact_amax(am, h)
+    dh = torch.randn(T, f, device="cuda", dtype=torch.bfloat16)
+    h.backward(dh)
+    hf.backward(dh.float())
+    close_bf16(gu.grad, gf.grad, rtol=2 ** -6, atol=1e-3)
+
+
+@pytest.mark.parametrize("B,S,H,hd", [(1, 64, 4, 32), (2, 256, 12, 64), (1, 1024, 32, 128)])
+def test_rope_fwd_bwd(B, S, H, hd):
+    torch.manual_seed(S)
+    cfg = L.LlamaConfig(d_model=H * hd, n_heads=H, max_seq=S)
+    cos, sin = L._rope_tables(cfg, "cuda")
+    qkv = torch.randn(B, S, 3 * H * hd, device="cuda", dtype=torch.bfloat16).requires_grad_(True)
+    q, k, v = RopeQKVFn.apply(qkv, cos, sin, H, None)
+    qf = qkv.detach().float().requires_grad_(True)
+    d = H * hd
+    qr, kr, vr = qf.split(d, dim=-1)
+    tr = lambda t: t.view(B, S, H, hd).transpose(1, 2)
+    q_ref = L._apply_rope(tr(qr), cos, sin)
+    k_ref = L._apply_rope(tr(kr), cos, sin)
+    close_bf16(q, q_ref, atol=1e-4)
+    close_bf16(k, k_ref, atol=1e-4)
+    assert torch.equal(v, tr(qkv.detach()[..., 2 * d:]))
+    gq, gk, gv = (torch.randn(B, H, S, hd, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    torch.autograd.backward([q, k, v], [gq, gk, gv])
+    torch.autograd.backward([q_ref, k_ref, tr(vr)], [gq.float(), gk.float(), gv.float()])
+    close_bf16(qkv.grad, qf.grad, rtol=2 ** -6, atol=1e-3)
+
+
+def test_fused_block_matches_torch_glue_and_uses_producer_amax(monkeypatch):
+    """Same weights, same input: the fused block (producer kernels) and the
+    torch-glue block give the same loss and gradients up to bf16 rounding, and
+    every quantizer except the O-proj input runs in producer-amax mode."""
+    cfg = L.LlamaConfig(vocab=512, d_model=256, n_layers=2, n_heads=4, d_ffn=512, max_seq=128)
+    torch.manual_seed(0)
+    m_fused = L.LlamaModel(cfg)
+    m_glue = L.LlamaModel(L.LlamaConfig(**{**cfg.__dict__, "fused_ops": False}))
+    m_glue.load_state_dict(m_fused.state_dict())
+    tok = torch.randint(0, cfg.vocab, (2, 129), device="cuda")
+    given = []
+    from paper_2511_05811_b200 import quantize as Q
+    orig = Q.quantize_mx2
+
+    def spy(x2d, **kw):
+        given.append(kw.get("amax") is not None)
+        return orig(x2d, **kw)
+    monkeypatch.setattr(mnn, "quantize_mx2", spy)
+    losses, grads = [], []
+    for m in (m_fused, m_glue):
+        given.clear()
+        loss = m(tok[:, :-1], tok[:, 1:])
+        loss.backward()
+        losses.append(float(loss))
+        grads.append({n: (p.main_grad if hasattr(p, "moss_layer") else p.grad).clone() for n, p in m.named_parameters()})
+        if m is m_fused:
+            n_given = sum(given)
+            # forward: qkv, gate_up, down given (o not); backward: all four given
+            assert n_given == 2 * (3 + 4), given
+    assert abs(losses[0] - losses[1]) <= 2e-3 * abs(losses[1])
+    # the two paths round activations differently (one bf16 rounding per fused
+    # op vs one per torch op), which moves FP8 codes: gradients agree to the
+    # FP8 quantization noise (~2^-4 per element), not to bf16 rounding
+    for n in grads[0]:
+        a, b = grads[0][n].float().flatten(), grads[1][n].float().flatten()
+        rel = float((a - b).norm() / (b.norm() + 1e-12))
+        cos = float(torch.dot(a, b) / (a.norm() * b.norm() + 1e-12))
+        assert rel < 0.15 and cos > 0.99, (n, rel, cos)
+    mnn.raise_if_flagged("cuda", "fused block")
