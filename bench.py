@@ -248,11 +248,19 @@ def main() -> None:
     opt.check("warmup")
     barrier()
 
-    # ---- per-kernel timing pass (eager, every launch bracketed by CUDA events)
+    # ---- per-kernel timing pass (eager, every launch bracketed by CUDA events).
+    # A device-side sleep ahead of each step lets the host enqueue the whole
+    # step first, so the events bracket GPU time only (no host launch gaps).
+    h0 = time.perf_counter()
+    step(x)
+    torch.cuda.synchronize()
+    issue_ms = (time.perf_counter() - h0) * 1e3
+    sleep_cycles = int(issue_ms * 2.5 * 2.0e6)          # ~2.5x the host issue time at ~2 GHz
     _lib.INSTR.start(timing=True)
     for _ in range(args.steps):
+        torch.cuda._sleep(sleep_cycles)
         step(x)
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
     _lib.INSTR.stop()
     kern = _lib.INSTR.summary()
     launches = _lib.INSTR.launches // args.steps
@@ -376,12 +384,15 @@ def main() -> None:
         "roofline": {"bound": "tensor", "kernel": "moss::gemm_mxf8_2cta_kernel (tcgen05.mma.cta_group::2 kind::mxf8f6f4.block_scale)",
                      "achieved": gemm_tflops, "peak": fp8_peak, "unit": "TFLOP/s", "frac": gemm_tflops / fp8_peak,
                      "peak_source": "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (fp8 dense = 2x bf16)",
-                     "frac_of_burst": gemm_tflops / (2.0 * bf16_burst), "traffic": traffic,
+                     "frac_of_burst": gemm_tflops / (2.0 * bf16_burst),
+                     "frac_of_nominal_4500": gemm_tflops / 4500.0, "traffic": traffic,
                      "share_of_step": (g["ms"] / args.steps) / ms if g["launches"] else None},
         "kernels": {"quantize": rate("quant"), "amax": rate("amax"), "adamw_fp8": rate("adamw"),
+                    "producers": rate("producer"),
                     "gemm_ms_per_step": g["ms"] / args.steps, "all_kernels_ms_per_step": total_kernel_ms,
                     "host_issue_ms_per_step": host_ms,
-                    "timing_source": "per-kernel CUDA events from an instrumented eager pass of the same step; "
+                    "timing_source": "per-kernel CUDA events from an instrumented eager pass of the same step "
+                                     "(device sleep ahead of each step: no host gaps inside the events); "
                                      "value/ms_per_step from " + ("CUDA-graph replays" if use_graph else "eager steps")},
         "e2e": e2e,
     }

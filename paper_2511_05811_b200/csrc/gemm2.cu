@@ -57,6 +57,21 @@ struct G2Layout {
     static constexpr uint32_t TMEM_COLS = 512;                 // 256 accumulator + SF columns
 };
 
+// Tile raster: groups of G2_GROUP_M m-pairs walked n-major, so the ~74
+// concurrently running pair tiles share a 2048-row A panel and a few B panels
+// (both L2-resident); a plain m-major walk re-read all of A from DRAM for every
+// n column on tall problems (12288 x 4096 x 8192: 49 % DRAM, 4x the bytes).
+constexpr int G2_GROUP_M = 8;
+__device__ __forceinline__ void g2_tile_coords(int tile, int m_pairs, int n_tiles, int& mp, int& nt) {
+    const int group = G2_GROUP_M * n_tiles;
+    const int gi = tile / group;
+    const int first = gi * G2_GROUP_M;
+    const int gm = min(m_pairs - first, G2_GROUP_M);
+    const int r = tile - gi * group;
+    mp = first + r % gm;
+    nt = r / gm;
+}
+
 // SF buffers are viewed as [bytes/256, 256] u8 tensors: one 512 B chunk = box {256, 2}
 __device__ __forceinline__ int sf_row_of_chunk(int64_t chunk) { return (int)(chunk * 2); }
 
@@ -127,7 +142,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
         int stage = 0;
         uint32_t phase = 0;
         for (int tile = pair; tile < num_tiles; tile += npairs) {
-            const int mp = tile % m_pairs, nt = tile / m_pairs;
+            int mp, nt;
+            g2_tile_coords(tile, m_pairs, n_tiles, mp, nt);
             const int mb = mp * 2 + rank;                       // this CTA's 128-row block of A
             const int n0 = nt * G2_BN + rank * (G2_BN / 2);     // this CTA's half of B
             for (int kb = 0; kb < kblocks; ++kb) {
@@ -218,7 +234,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
         const float alpha = __fmul_rn(*sA, *sB);
         uint32_t acc_phase = 0;
         for (int tile = pair; tile < num_tiles; tile += npairs) {
-            const int mp = tile % m_pairs, nt = tile / m_pairs;
+            int mp, nt;
+            g2_tile_coords(tile, m_pairs, n_tiles, mp, nt);
             const int row0 = (mp * 2 + rank) * G2_BM + quad * 32;
             const int col0 = nt * G2_BN + cq * COLS;
             mbar_wait(tmem_full, acc_phase);
