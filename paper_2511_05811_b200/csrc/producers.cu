@@ -24,6 +24,15 @@ namespace moss {
 
 __device__ __forceinline__ void bf16x8_load(const __nv_bfloat16* p, float (&v)[8]) { Vec8<__nv_bfloat16>::load(p, v); }
 
+__device__ __forceinline__ void unpack_bf16x8(const uint4& u, float (&v)[8]) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        v[2 * i] = __uint_as_float(w[i] << 16);
+        v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+}
+
 __device__ __forceinline__ uint4 bf16x8_pack(const float (&v)[8]) {
     uint4 o;
     o.x = pack_bf16(v[0], v[1]);
@@ -80,7 +89,7 @@ __device__ __forceinline__ void block_amax_commit(uint32_t m, uint32_t* red_u, u
 //   y  = bf16( f32(x') * rsqrt(mean(f32(x')^2) + eps) * w )
 //   rstd[t] = rsqrt(...), amax = max |y|
 template <int NT>
-__global__ void __launch_bounds__(NT) rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+__global__ void __launch_bounds__(NT, (1024 / NT > 0 ? 1024 / NT : 1)) rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x,
                                                          const __nv_bfloat16* __restrict__ delta,
                                                          __nv_bfloat16* __restrict__ x_out, const float* __restrict__ w,
                                                          float eps, __nv_bfloat16* __restrict__ y,
@@ -96,15 +105,27 @@ __global__ void __launch_bounds__(NT) rmsnorm_fwd_kernel(const __nv_bfloat16* __
         wv[0] = a.x; wv[1] = a.y; wv[2] = a.z; wv[3] = a.w; wv[4] = b.x; wv[5] = b.y; wv[6] = b.z; wv[7] = b.w;
     }
     uint32_t m = 0;
+    // one row of look-ahead: the next row's loads are in flight during this row's reduction
+    uint4 xa = make_uint4(0, 0, 0, 0), da = make_uint4(0, 0, 0, 0);
+    auto load = [&](int t, uint4& xr, uint4& dr) {
+        if (act && t < T) {
+            const int64_t off = (int64_t)t * d + c;
+            xr = *reinterpret_cast<const uint4*>(x + off);
+            if (delta) dr = *reinterpret_cast<const uint4*>(delta + off);
+        }
+    };
+    load(blockIdx.x, xa, da);
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
         const int64_t off = (int64_t)t * d + c;
+        uint4 xn = make_uint4(0, 0, 0, 0), dn = make_uint4(0, 0, 0, 0);
+        load(t + gridDim.x, xn, dn);
         float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         float ss = 0.f;
         if (act) {
-            bf16x8_load(x + off, v);
+            unpack_bf16x8(xa, v);
             if (delta) {
                 float dv[8];
-                bf16x8_load(delta + off, dv);
+                unpack_bf16x8(da, dv);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i] + dv[i]));
                 *reinterpret_cast<uint4*>(x_out + off) = bf16x8_pack(v);
@@ -123,6 +144,8 @@ __global__ void __launch_bounds__(NT) rmsnorm_fwd_kernel(const __nv_bfloat16* __
             *reinterpret_cast<uint4*>(y + off) = ob;
             m = max(m, absmax_bits_bf16(ob));
         }
+        xa = xn;
+        da = dn;
     }
     block_amax_commit(m, red_u, amax);
 }
@@ -134,7 +157,7 @@ __global__ void __launch_bounds__(NT) rmsnorm_fwd_kernel(const __nv_bfloat16* __
 //        reduction: deterministic, so replays and DP ranks agree bit for bit)
 //   amax = max |dx|
 template <int NT>
-__global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
+__global__ void __launch_bounds__(NT, (1024 / NT > 0 ? 1024 / NT : 1)) rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
                                                          const __nv_bfloat16* __restrict__ x,
                                                          const float* __restrict__ w, const float* __restrict__ rstd,
                                                          const __nv_bfloat16* __restrict__ d_res,
@@ -152,15 +175,27 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(const __nv_bfloat16* __
     }
     uint32_t m = 0;
     const float inv_d = 1.0f / (float)d;
+    uint4 ya = make_uint4(0, 0, 0, 0), xa = ya, ra = ya;
+    auto load = [&](int t, uint4& yr, uint4& xr, uint4& rr) {
+        if (act && t < T) {
+            const int64_t off = (int64_t)t * d + c;
+            yr = *reinterpret_cast<const uint4*>(dy + off);
+            xr = *reinterpret_cast<const uint4*>(x + off);
+            if (d_res) rr = *reinterpret_cast<const uint4*>(d_res + off);
+        }
+    };
+    load(blockIdx.x, ya, xa, ra);
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
         const int64_t off = (int64_t)t * d + c;
+        uint4 yn = make_uint4(0, 0, 0, 0), xn = yn, rn = yn;
+        load(t + gridDim.x, yn, xn, rn);
         const float r = rstd[t];
         float g[8], xh[8];
         float dot = 0.f;
         if (act) {
             float dv[8];
-            bf16x8_load(dy + off, dv);
-            bf16x8_load(x + off, xh);
+            unpack_bf16x8(ya, dv);
+            unpack_bf16x8(xa, xh);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 xh[i] *= r;
@@ -176,7 +211,7 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(const __nv_bfloat16* __
             for (int i = 0; i < 8; ++i) o[i] = r * (g[i] - xh[i] * dot);
             if (d_res) {
                 float rv[8];
-                bf16x8_load(d_res + off, rv);
+                unpack_bf16x8(ra, rv);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) o[i] += rv[i];
             }
@@ -184,6 +219,9 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(const __nv_bfloat16* __
             *reinterpret_cast<uint4*>(dx + off) = ob;
             m = max(m, absmax_bits_bf16(ob));
         }
+        ya = yn;
+        xa = xn;
+        ra = rn;
     }
     if (act && dw_part) {   // this CTA's column sums; reduced in a fixed order by rmsnorm_dw_reduce_kernel
         float* dst = dw_part + (int64_t)blockIdx.x * d + c;
@@ -193,35 +231,47 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(const __nv_bfloat16* __
     block_amax_commit(m, red_u, amax);
 }
 
-// dw[c] += sum_b part[b, c] in order b = 0, 1, ...
-__global__ void __launch_bounds__(256) rmsnorm_dw_reduce_kernel(const float* __restrict__ part, float* __restrict__ dw,
-                                                                int nb, int d) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= d) return;
+// dw[c] += sum_b part[b, c]: thread (cx, ry) of a 64 x 16 block sums rows
+// ry, ry+16, ... of column c, then the 16 partial sums are added in ry order
+// (a fixed order: deterministic).
+__global__ void __launch_bounds__(1024) rmsnorm_dw_reduce_kernel(const float* __restrict__ part, float* __restrict__ dw,
+                                                                 int nb, int d) {
+    __shared__ float red[16][64];
+    const int cx = threadIdx.x & 63, ry = threadIdx.x >> 6;
+    const int c = blockIdx.x * 64 + cx;
     float s = 0.f;
-    for (int b = 0; b < nb; ++b) s += part[(int64_t)b * d + c];
-    dw[c] += s;
+    if (c < d)
+        for (int b = ry; b < nb; b += 16) s += part[(int64_t)b * d + c];
+    red[ry][cx] = s;
+    __syncthreads();
+    if (ry == 0 && c < d) {
+        float t = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) t += red[i][cx];
+        dw[c] += t;
+    }
 }
 
 // ------------------------------------------------------------------ SwiGLU
 // gu [T, 2f] = [gate | up];  h = bf16( silu(g) * u ),  amax = max |h|
+// grid (column chunks, row groups); each thread one 8-element vector per row
 __global__ void __launch_bounds__(256) swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu,
                                                          __nv_bfloat16* __restrict__ h, uint32_t* amax, int64_t T,
                                                          int f) {
     __shared__ uint32_t red_u[8];
-    const int64_t nv = T * (f / 8);
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
     uint32_t m = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t = i / (f / 8);
-        const int c = (int)(i - t * (f / 8)) * 8;
-        float g[8], u[8], o[8];
-        bf16x8_load(gu + t * 2 * f + c, g);
-        bf16x8_load(gu + t * 2 * f + f + c, u);
+    if (c < f) {
+        for (int64_t t = blockIdx.y; t < T; t += gridDim.y) {
+            float g[8], u[8], o[8];
+            bf16x8_load(gu + t * 2 * f + c, g);
+            bf16x8_load(gu + t * 2 * f + f + c, u);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) o[k] = g[k] / (1.0f + __expf(-g[k])) * u[k];
-        const uint4 ob = bf16x8_pack(o);
-        *reinterpret_cast<uint4*>(h + t * f + c) = ob;
-        m = max(m, absmax_bits_bf16(ob));
+            for (int k = 0; k < 8; ++k) o[k] = __fdividef(g[k], 1.0f + __expf(-g[k])) * u[k];
+            const uint4 ob = bf16x8_pack(o);
+            *reinterpret_cast<uint4*>(h + t * f + c) = ob;
+            m = max(m, absmax_bits_bf16(ob));
+        }
     }
     block_amax_commit(m, red_u, amax);
 }
@@ -232,25 +282,25 @@ __global__ void __launch_bounds__(256) swiglu_bwd_kernel(const __nv_bfloat16* __
                                                          __nv_bfloat16* __restrict__ dgu, uint32_t* amax, int64_t T,
                                                          int f) {
     __shared__ uint32_t red_u[8];
-    const int64_t nv = T * (f / 8);
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
     uint32_t m = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t = i / (f / 8);
-        const int c = (int)(i - t * (f / 8)) * 8;
-        float g[8], u[8], d[8], og[8], ou[8];
-        bf16x8_load(gu + t * 2 * f + c, g);
-        bf16x8_load(gu + t * 2 * f + f + c, u);
-        bf16x8_load(dh + t * f + c, d);
+    if (c < f) {
+        for (int64_t t = blockIdx.y; t < T; t += gridDim.y) {
+            float g[8], u[8], d[8], og[8], ou[8];
+            bf16x8_load(gu + t * 2 * f + c, g);
+            bf16x8_load(gu + t * 2 * f + f + c, u);
+            bf16x8_load(dh + t * f + c, d);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const float s = 1.0f / (1.0f + __expf(-g[k]));
-            og[k] = d[k] * u[k] * s * (1.0f + g[k] * (1.0f - s));
-            ou[k] = d[k] * g[k] * s;
+            for (int k = 0; k < 8; ++k) {
+                const float s = __fdividef(1.0f, 1.0f + __expf(-g[k]));
+                og[k] = d[k] * u[k] * s * (1.0f + g[k] * (1.0f - s));
+                ou[k] = d[k] * g[k] * s;
+            }
+            const uint4 a = bf16x8_pack(og), b = bf16x8_pack(ou);
+            *reinterpret_cast<uint4*>(dgu + t * 2 * f + c) = a;
+            *reinterpret_cast<uint4*>(dgu + t * 2 * f + f + c) = b;
+            m = max(m, max(absmax_bits_bf16(a), absmax_bits_bf16(b)));
         }
-        const uint4 a = bf16x8_pack(og), b = bf16x8_pack(ou);
-        *reinterpret_cast<uint4*>(dgu + t * 2 * f + c) = a;
-        *reinterpret_cast<uint4*>(dgu + t * 2 * f + f + c) = b;
-        m = max(m, max(absmax_bits_bf16(a), absmax_bits_bf16(b)));
     }
     block_amax_commit(m, red_u, amax);
 }
@@ -263,34 +313,32 @@ __global__ void __launch_bounds__(256) rope_fwd_kernel(const __nv_bfloat16* __re
                                                        const float* __restrict__ cosv, const float* __restrict__ sinv,
                                                        __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ k,
                                                        __nv_bfloat16* __restrict__ v, int B, int S, int H, int hd) {
-    const int vh = hd / 8;   // 8-element vectors per head
-    const int64_t nv = (int64_t)B * S * H * vh;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
-        const int j = (int)(i % vh);
-        const int64_t r = i / vh;
-        const int h = (int)(r % H);
-        const int64_t bs = r / H;
-        const int s = (int)(bs % S);
-        const int b = (int)(bs / S);
-        const int64_t src = bs * 3 * H * hd + (int64_t)h * hd + j * 8;
-        const int64_t dst = (((int64_t)b * H + h) * S + s) * hd + j * 8;
-        const float* cs = cosv + (int64_t)s * (hd / 2) + j * 4;
-        const float* sn = sinv + (int64_t)s * (hd / 2) + j * 4;
-        float qa[8], ka[8], qo[8], ko[8];
-        bf16x8_load(qkv + src, qa);
-        bf16x8_load(qkv + src + (int64_t)H * hd, ka);
+    // blockIdx.x = token (b, s); (blockIdx.y, thread) cover the H*hd/8 vectors of q, k and v
+    const int vh = hd / 8;
+    const int i = blockIdx.y * blockDim.x + threadIdx.x;
+    if (i >= H * vh) return;
+    const int bs = blockIdx.x;
+    const int s = bs % S, b = bs / S;
+    const int h = i / vh, j = i - h * vh;
+    const int64_t src = (int64_t)bs * 3 * H * hd + (int64_t)i * 8;
+    const int64_t dst = (((int64_t)b * H + h) * S + s) * hd + j * 8;
+    const float4 c4 = *reinterpret_cast<const float4*>(cosv + (int64_t)s * (hd / 2) + j * 4);
+    const float4 s4 = *reinterpret_cast<const float4*>(sinv + (int64_t)s * (hd / 2) + j * 4);
+    const float cs[4] = {c4.x, c4.y, c4.z, c4.w}, sn[4] = {s4.x, s4.y, s4.z, s4.w};
+    float qa[8], ka[8], qo[8], ko[8];
+    bf16x8_load(qkv + src, qa);
+    bf16x8_load(qkv + src + (int64_t)H * hd, ka);
+    const uint4 vv = *reinterpret_cast<const uint4*>(qkv + src + 2 * (int64_t)H * hd);
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            const float c = cs[p], sv = sn[p];
-            qo[2 * p] = qa[2 * p] * c - qa[2 * p + 1] * sv;
-            qo[2 * p + 1] = qa[2 * p] * sv + qa[2 * p + 1] * c;
-            ko[2 * p] = ka[2 * p] * c - ka[2 * p + 1] * sv;
-            ko[2 * p + 1] = ka[2 * p] * sv + ka[2 * p + 1] * c;
-        }
-        *reinterpret_cast<uint4*>(q + dst) = bf16x8_pack(qo);
-        *reinterpret_cast<uint4*>(k + dst) = bf16x8_pack(ko);
-        *reinterpret_cast<uint4*>(v + dst) = *reinterpret_cast<const uint4*>(qkv + src + 2 * (int64_t)H * hd);
+    for (int p = 0; p < 4; ++p) {
+        qo[2 * p] = qa[2 * p] * cs[p] - qa[2 * p + 1] * sn[p];
+        qo[2 * p + 1] = qa[2 * p] * sn[p] + qa[2 * p + 1] * cs[p];
+        ko[2 * p] = ka[2 * p] * cs[p] - ka[2 * p + 1] * sn[p];
+        ko[2 * p + 1] = ka[2 * p] * sn[p] + ka[2 * p + 1] * cs[p];
     }
+    *reinterpret_cast<uint4*>(q + dst) = bf16x8_pack(qo);
+    *reinterpret_cast<uint4*>(k + dst) = bf16x8_pack(ko);
+    *reinterpret_cast<uint4*>(v + dst) = vv;
 }
 
 // dq, dk, dv [B, H, S, hd] -> dqkv [B, S, 3, H, hd] (inverse rotation), amax = max |dqkv|
@@ -302,43 +350,49 @@ __global__ void __launch_bounds__(256) rope_bwd_kernel(const __nv_bfloat16* __re
                                                        int H, int hd) {
     __shared__ uint32_t red_u[8];
     const int vh = hd / 8;
-    const int64_t nv = (int64_t)B * S * H * vh;
+    const int i = blockIdx.y * blockDim.x + threadIdx.x;
     uint32_t m = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
-        const int j = (int)(i % vh);
-        const int64_t r = i / vh;
-        const int h = (int)(r % H);
-        const int64_t bs = r / H;
-        const int s = (int)(bs % S);
-        const int b = (int)(bs / S);
-        const int64_t dst = bs * 3 * H * hd + (int64_t)h * hd + j * 8;
+    if (i < H * vh) {
+        const int bs = blockIdx.x;
+        const int s = bs % S, b = bs / S;
+        const int h = i / vh, j = i - h * vh;
+        const int64_t dst = (int64_t)bs * 3 * H * hd + (int64_t)i * 8;
         const int64_t src = (((int64_t)b * H + h) * S + s) * hd + j * 8;
-        const float* cs = cosv + (int64_t)s * (hd / 2) + j * 4;
-        const float* sn = sinv + (int64_t)s * (hd / 2) + j * 4;
+        const float4 c4 = *reinterpret_cast<const float4*>(cosv + (int64_t)s * (hd / 2) + j * 4);
+        const float4 s4 = *reinterpret_cast<const float4*>(sinv + (int64_t)s * (hd / 2) + j * 4);
+        const float cs[4] = {c4.x, c4.y, c4.z, c4.w}, sn[4] = {s4.x, s4.y, s4.z, s4.w};
         float qa[8], ka[8], qo[8], ko[8];
         bf16x8_load(dq + src, qa);
         bf16x8_load(dk + src, ka);
+        const uint4 vv = *reinterpret_cast<const uint4*>(dv + src);
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-            const float c = cs[p], sv = sn[p];
-            qo[2 * p] = qa[2 * p] * c + qa[2 * p + 1] * sv;
-            qo[2 * p + 1] = -qa[2 * p] * sv + qa[2 * p + 1] * c;
-            ko[2 * p] = ka[2 * p] * c + ka[2 * p + 1] * sv;
-            ko[2 * p + 1] = -ka[2 * p] * sv + ka[2 * p + 1] * c;
+            qo[2 * p] = qa[2 * p] * cs[p] + qa[2 * p + 1] * sn[p];
+            qo[2 * p + 1] = -qa[2 * p] * sn[p] + qa[2 * p + 1] * cs[p];
+            ko[2 * p] = ka[2 * p] * cs[p] + ka[2 * p + 1] * sn[p];
+            ko[2 * p + 1] = -ka[2 * p] * sn[p] + ka[2 * p + 1] * cs[p];
         }
         const uint4 a = bf16x8_pack(qo), bb = bf16x8_pack(ko);
-        const uint4 vv = *reinterpret_cast<const uint4*>(dv + src);
         *reinterpret_cast<uint4*>(dqkv + dst) = a;
         *reinterpret_cast<uint4*>(dqkv + dst + (int64_t)H * hd) = bb;
         *reinterpret_cast<uint4*>(dqkv + dst + 2 * (int64_t)H * hd) = vv;
-        m = max(m, max(absmax_bits_bf16(a), max(absmax_bits_bf16(bb), absmax_bits_bf16(vv))));
+        m = max(absmax_bits_bf16(a), max(absmax_bits_bf16(bb), absmax_bits_bf16(vv)));
     }
     block_amax_commit(m, red_u, amax);
 }
 
 // ------------------------------------------------------------------ launchers
-static int grid_for(int64_t work, int threads, int per_sm) {
-    return (int)std::max<int64_t>(1, std::min<int64_t>((work + threads - 1) / threads, (int64_t)sm_count() * per_sm));
+template <typename K>
+static int resident(K kern, int threads) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, 0) != cudaSuccess || occ < 1) occ = 1;
+    return occ;
+}
+
+static dim3 swiglu_grid(int64_t T, int64_t f) {
+    const int64_t gx = (f / 8 + 255) / 256;
+    const int64_t gy = std::min<int64_t>(T, std::max<int64_t>(1, (int64_t)sm_count() * 16 / gx));
+    return dim3((unsigned)gx, (unsigned)gy);
 }
 
 static int amax_reset(uint32_t* amax, cudaStream_t st) {
@@ -349,8 +403,9 @@ int launch_rmsnorm_fwd(const void* x, const void* delta, void* x_out, const floa
                        float* amax, int64_t T, int64_t d, cudaStream_t st) {
     if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
     const int nt = (int)((d / 8 + 31) / 32 * 32);
-    const int grid = (int)std::min<int64_t>(T, (int64_t)sm_count() * (2048 / nt));
     auto args = [&](auto kern) {
+        static int occ = resident(kern, nt);     // one static per template instance
+        const int grid = (int)std::min<int64_t>(T, (int64_t)sm_count() * occ);
         kern<<<grid, nt, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)delta,
                                                   (__nv_bfloat16*)x_out, w, eps, (__nv_bfloat16*)y, rstd,
                                                   reinterpret_cast<uint32_t*>(amax), (int)T, (int)d);
@@ -395,20 +450,20 @@ int launch_rmsnorm_bwd(const void* dy, const void* x, const float* w, const floa
         case 1024: args(rmsnorm_bwd_kernel<1024>); break;
         default: return MOSS_ERR_SHAPE;
     }
-    if (dw) rmsnorm_dw_reduce_kernel<<<(unsigned)((d + 255) / 256), 256, 0, st>>>(ws, dw, grid, (int)d);
+    if (dw) rmsnorm_dw_reduce_kernel<<<(unsigned)((d + 63) / 64), 1024, 0, st>>>(ws, dw, grid, (int)d);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 
 int launch_swiglu_fwd(const void* gu, void* h, float* amax, int64_t T, int64_t f, cudaStream_t st) {
     if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
-    swiglu_fwd_kernel<<<grid_for(T * (f / 8), 256, 8), 256, 0, st>>>(
+    swiglu_fwd_kernel<<<swiglu_grid(T, f), 256, 0, st>>>(
         (const __nv_bfloat16*)gu, (__nv_bfloat16*)h, reinterpret_cast<uint32_t*>(amax), T, (int)f);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 
 int launch_swiglu_bwd(const void* dh, const void* gu, void* dgu, float* amax, int64_t T, int64_t f, cudaStream_t st) {
     if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
-    swiglu_bwd_kernel<<<grid_for(T * (f / 8), 256, 8), 256, 0, st>>>(
+    swiglu_bwd_kernel<<<swiglu_grid(T, f), 256, 0, st>>>(
         (const __nv_bfloat16*)dh, (const __nv_bfloat16*)gu, (__nv_bfloat16*)dgu, reinterpret_cast<uint32_t*>(amax), T,
         (int)f);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
@@ -416,7 +471,7 @@ int launch_swiglu_bwd(const void* dh, const void* gu, void* dgu, float* amax, in
 
 int launch_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q, void* k, void* v, int64_t B,
                     int64_t S, int64_t H, int64_t hd, cudaStream_t st) {
-    rope_fwd_kernel<<<grid_for(B * S * H * (hd / 8), 256, 8), 256, 0, st>>>(
+    rope_fwd_kernel<<<dim3((unsigned)(B * S), (unsigned)((H * (hd / 8) + 255) / 256)), 256, 0, st>>>(
         (const __nv_bfloat16*)qkv, cosv, sinv, (__nv_bfloat16*)q, (__nv_bfloat16*)k, (__nv_bfloat16*)v, (int)B, (int)S,
         (int)H, (int)hd);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
@@ -425,7 +480,7 @@ int launch_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void*
 int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
                     float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, cudaStream_t st) {
     if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
-    rope_bwd_kernel<<<grid_for(B * S * H * (hd / 8), 256, 8), 256, 0, st>>>(
+    rope_bwd_kernel<<<dim3((unsigned)(B * S), (unsigned)((H * (hd / 8) + 255) / 256)), 256, 0, st>>>(
         (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv, cosv, sinv,
         (__nv_bfloat16*)dqkv, reinterpret_cast<uint32_t*>(amax), (int)B, (int)S, (int)H, (int)hd);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
