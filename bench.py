@@ -42,7 +42,7 @@ METRIC = "FP8 GEMM TFLOP/s, quantize GB/s; 7B-shape train tokens/s at 1/2/4/8 B2
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--tokens", type=int, default=8192)
@@ -124,52 +124,110 @@ def run_reference(args, rank: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ library reference for the GEMM roofline
+def gemm_vs_cublas(dev, tokens: int) -> dict | None:
+    """Our K2 and cuBLASLt MXFP8 (torch F.scaled_mm, BlockWise1x32) on the same
+    codes/scales for the 12 GEMMs of one layer step (fwd, dgrad, wgrad of the
+    Llama-7B linears); FLOP-weighted TFLOP/s of each, back-to-back launches
+    timed with CUDA events (device time only).  cuBLAS is a library
+    measurement of this box's attainable MXFP8 rate, not part of the product."""
+    import torch
+    import torch.nn.functional as F
+
+    from paper_2511_05811_b200.gemm import mx_gemm
+    from paper_2511_05811_b200.quantize import quantize_mx2
+    if not hasattr(F, "scaled_mm"):
+        return None
+    shapes = []
+    for k, n in [(4096, 12288), (4096, 4096), (4096, 22016), (11008, 4096)]:
+        shapes += [(tokens, n, k), (tokens, k, n), (n, k, tokens)]
+    one = torch.ones(1, device=dev)
+    t_ours = t_cub = flops = 0.0
+    for (m, n, k) in shapes:
+        a = torch.randn(m, k, device=dev, dtype=torch.bfloat16)
+        b = torch.randn(n, k, device=dev, dtype=torch.bfloat16)
+        qa, qb = quantize_mx2(a), quantize_mx2(b)
+        out = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
+        A8, B8 = qa.codes.view(torch.float8_e4m3fn), qb.codes.view(torch.float8_e4m3fn).t()
+        sa, sb = qa.sf.view(torch.float8_e8m0fnu), qb.sf.view(torch.float8_e8m0fnu)
+
+        def ours():
+            mx_gemm(qa.codes, qa.sf, one, qb.codes, qb.sf, one, out=out)
+
+        def cub():
+            F.scaled_mm(A8, B8, sa, F.ScalingType.BlockWise1x32, sb, F.ScalingType.BlockWise1x32,
+                        swizzle_a=F.SwizzleType.SWIZZLE_32_4_4, swizzle_b=F.SwizzleType.SWIZZLE_32_4_4,
+                        output_dtype=torch.bfloat16)
+        res = []
+        for fn in (ours, cub):
+            for _ in range(3):
+                fn()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for _ in range(10):
+                fn()
+            e.record()
+            torch.cuda.synchronize()
+            res.append(s.elapsed_time(e) / 10)
+        t_ours += res[0]
+        t_cub += res[1]
+        flops += 2.0 * m * n * k
+        del a, b, qa, qb, out
+    return {"ours_tflops": flops / (t_ours / 1e3) / 1e12, "cublas_mxfp8_tflops": flops / (t_cub / 1e3) / 1e12,
+            "ours_over_cublas": t_cub / t_ours,
+            "how": "12 layer GEMMs (fwd/dgrad/wgrad of QKV, O, gate_up, down) at M=%d, same codes and E8M0 scales, "
+                   "10 back-to-back launches each, CUDA events; cuBLASLt via torch F.scaled_mm" % tokens}
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled DURING the timed region (NVML in a
+    background thread every 20 ms; nvidia-smi is the fallback)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
-        self.rows: list[list[str]] = []
-        self.proc = None
+        self.samples: list[tuple[float, int]] = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.th = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.th = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append((float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                                             int(get_reasons(h))))
+                    except Exception:  # noqa: BLE001
+                        pass
+                    self._stop.wait(0.02)
+            self.th = threading.Thread(target=run, daemon=True)
             self.th.start()
-        except OSError:
-            self.proc = None
+        except Exception:  # noqa: BLE001 - no NVML: no samples, reported as such
+            self.th = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
-                self.rows.append(parts)
-
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self.th is not None:
+            self.th.join(timeout=2)
         return False
 
     def summary(self) -> dict:
-        rows = [r for r in self.rows if r[0] == str(self.idx)] or self.rows
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(rows)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"], "samples": 0}
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(c for c, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "NVML, 20 ms period, timed region"}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -396,6 +454,13 @@ def main() -> None:
                                      "value/ms_per_step from " + ("CUDA-graph replays" if use_graph else "eager steps")},
         "e2e": e2e,
     }
+    if not llama:
+        try:
+            cmp = gemm_vs_cublas(dev, T)
+        except Exception as ex:  # noqa: BLE001 - a library comparison must not sink the bench line
+            cmp = {"error": str(ex)[:200]}
+        if cmp:
+            line["roofline"]["library_reference"] = cmp
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_sample(1024, 4096)
         line["cpu_baseline"].pop("seconds", None)

@@ -9,6 +9,10 @@ backward gradient:
     qkv = QKV(x); a = q + k + v              (stand-in for attention mixing)
     r = x + O(a); h = silu(gate(r)) * up(r); y = down(h); loss = mean(y^2)
 
+The SwiGLU is the producer kernel (producers.SwiGLUFn): it hands amax(h) to
+the down projection's quantizer and amax(dgu) to gate_up's backward, as in
+the Llama decoder.
+
 One step = forward + backward (FP8 fwd/dgrad/wgrad for every linear, each
 input and gradient two-level quantized row- and column-wise) + MossAdamW
 (fused update + autoscale + FP8 weight copy).  GEMM FLOPs per step:
@@ -18,10 +22,10 @@ input and gradient two-level quantized row- and column-wise) + MossAdamW
 from __future__ import annotations
 
 import torch
-import torch.nn.functional as F
 from torch import nn
 
 from .nn import MossLinear
+from .producers import SwiGLUFn
 
 LLAMA7B_SHAPES = {"qkv": (4096, 12288), "o": (4096, 4096), "gate_up": (4096, 22016), "down": (11008, 4096)}
 
@@ -39,8 +43,8 @@ class LayerStack(nn.Module):
         q, k, v = self.qkv(x).split(self.d, dim=-1)
         a = q + k + v
         r = x + self.o(a)
-        g, u = self.gate_up(r).split(self.f, dim=-1)
-        y = self.down(F.silu(g) * u)
+        h, am = SwiGLUFn.apply(self.gate_up(r), self.gate_up)
+        y = self.down(h, am)
         return (y.float() ** 2).mean()
 
     def gemm_flops_per_token(self) -> int:
