@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
+    ap.add_argument("--zero1", action="store_true",
+                    help="N>1: ZeRO-1 (reduce-scatter grads, sharded K3, FP8 all-gather) instead of all-reduce DP")
     return ap.parse_args()
 
 
@@ -242,6 +244,13 @@ def main() -> None:
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif args.zero1 and args.impl != "reference":
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
     if args.impl == "reference":
         run_reference(args, rank)
         if world > 1:
@@ -275,7 +284,11 @@ def main() -> None:
         x = torch.randn(T, model.d, device=dev, dtype=torch.bfloat16)
         flops_step = float(model.gemm_flops_per_token()) * T
         fwd = model
-    buckets = GradBuckets(model, bucket_mb=64) if world > 1 else None
+    if args.zero1:
+        from paper_2511_05811_b200.zero import Zero1
+        buckets = Zero1(opt, bucket_mb=64)
+    else:
+        buckets = GradBuckets(model, bucket_mb=64) if world > 1 else None
     if buckets is not None:
         opt.grad_scale = buckets.grad_scale
 
@@ -292,7 +305,10 @@ def main() -> None:
         else:
             opt.zero_grad()
         loss = fwd_bwd(xin)
-        opt.step()
+        if hasattr(buckets, "step"):
+            buckets.step()
+        else:
+            opt.step()
         return loss
 
     def barrier():
@@ -300,7 +316,7 @@ def main() -> None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    use_graph = world == 1 and not args.no_graph
+    use_graph = world == 1 and not args.no_graph and not args.zero1
     for _ in range(max(3, args.warmup)):
         step(x)
     opt.check("warmup")
@@ -432,7 +448,9 @@ def main() -> None:
         "dtype": "e4m3 x e4m3 -> fp32 accumulate (MXFP8, E8M0 block scales); bf16 activations; fp32 master/optimizer",
         "data": "synthetic (randn bf16 activations, N(0,0.02^2) weights, random init)",
         "config": {"workload": wl, "tokens_per_gpu": T, "global_batch_tokens": T * world,
-                   "parallelism": f"dp{world}" + (" (NCCL bucketed fp32 grad all-reduce)" if world > 1 else ""),
+                   "parallelism": f"dp{world}" + ((" (ZeRO-1: NCCL reduce-scatter fp32 grads, sharded K3, FP8 all-gather)"
+                                                   if args.zero1 else " (NCCL bucketed fp32 grad all-reduce)")
+                                                  if world > 1 else (" (ZeRO-1 driver)" if args.zero1 else "")),
                    "gemm_flops_per_step_per_gpu": flops_step,
                    "gemm_tflops_per_s_whole_step": world * flops_step / (ms / 1e3) / 1e12,
                    "l2": "not flushed: per-step working set ~3 GB >> 126 MB L2"},

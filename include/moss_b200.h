@@ -182,6 +182,11 @@ int moss_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q
 int moss_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
                   float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, void* stream);
 
+/* dst [cols, rows] = src [rows, cols]^T, u8 (E4M3 codes).  ZeRO-1 rebuilds
+ * the dgrad operand W_fp8^T locally after the FP8 all-gather of W_fp8
+ * (per-tensor codes commute with the transpose).  rows, cols % 16 == 0. */
+int moss_transpose_u8(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, void* stream);
+
 /* Human-readable status. */
 const char* moss_strerror(int status);
 

@@ -44,6 +44,7 @@ _SIGS = {
     "moss_swiglu_bwd": (_I, [_P, _P, _P, _P, _I64, _I64, _P]),
     "moss_rope_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
     "moss_rope_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
+    "moss_transpose_u8": (_I, [_P, _P, _I64, _I64, _P]),
     "moss_encode_scaled": (_I, [_P, _I, _I64, _I64, _P, _F, _I, _P, _P, _P, _P, _P, _P]),
     "moss_gemm_mxf8": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _I, _P]),
     "moss_adamw_fp8": (_I, [_P, _P, _I, _P, _P, _I64, _I64, ctypes.POINTER(AdamParams), _F, _P, _P, _P,
@@ -329,3 +330,9 @@ def rope_bwd(dq, dk, dv, cos, sin, dqkv, amax, B: int, S: int, H: int, hd: int) 
     with _Span("producer", B * S * 3 * H * hd * 4):
         check(lib().moss_rope_bwd(dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), cos.data_ptr(), sin.data_ptr(),
                                   dqkv.data_ptr(), ptr(amax), B, S, H, hd, stream()), "moss_rope_bwd")
+
+
+def transpose_u8(src: torch.Tensor, dst: torch.Tensor) -> None:
+    rows, cols = src.shape
+    with _Span("transpose", 2 * rows * cols):
+        check(lib().moss_transpose_u8(src.data_ptr(), dst.data_ptr(), rows, cols, stream()), "moss_transpose_u8")

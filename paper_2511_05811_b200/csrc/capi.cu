@@ -34,6 +34,7 @@ int launch_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void*
                     int64_t S, int64_t H, int64_t hd, cudaStream_t st);
 int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
                     float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, cudaStream_t st);
+int launch_transpose_u8(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t st);
 }  // namespace moss
 
 static inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
@@ -208,6 +209,13 @@ int moss_rope_bwd(const void* dq, const void* dk, const void* dv, const float* c
     if (!dq || !dk || !dv || !cosv || !sinv || !dqkv) return MOSS_ERR_ARGUMENT;
     if (!al16(dq) || !al16(dk) || !al16(dv) || !al16(cosv) || !al16(sinv) || !al16(dqkv)) return MOSS_ERR_ALIGN;
     return moss::launch_rope_bwd(dq, dk, dv, cosv, sinv, dqkv, amax, B, S, H, hd, (cudaStream_t)stream);
+}
+
+int moss_transpose_u8(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, void* stream) {
+    if (rows <= 0 || cols <= 0 || rows > 65535 * 64LL) return MOSS_ERR_SHAPE;
+    if (!src || !dst) return MOSS_ERR_ARGUMENT;
+    if (!aligned(src, 16) || !aligned(dst, 16) || cols % 16 || rows % 16) return MOSS_ERR_ALIGN;
+    return moss::launch_transpose_u8(src, dst, rows, cols, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -290,6 +290,8 @@ class MossAdamW:
         self.grad_scale = 1.0
         dev = self.params[0].device
         self.state = {id(p): (torch.zeros_like(p), torch.zeros_like(p)) for p in self.params}
+        self.index = {id(p): i for i, p in enumerate(self.params)}
+        self.sharded: set[int] = set()      # parameters whose update is done elsewhere (zero.Zero1)
         self.saturations = torch.zeros(1, dtype=torch.int32, device=dev)
         self.rescale_events: list[tuple[int, int]] = []
         n = len(self.params)
@@ -298,6 +300,18 @@ class MossAdamW:
         self._ring_events: list = [None] * self._RING
         self._slot = 0
         self._rescale_pending = False
+
+    def shard(self, params) -> None:
+        """Hand the update of ``params`` to a sharded driver (zero.Zero1): their
+        moments are not kept here, ``launch`` skips them; ``prepare`` still
+        advances their schedules and stages their kernel arguments."""
+        for p in params:
+            self.sharded.add(id(p))
+            self.state[id(p)] = None
+
+    def record_ptr(self, p) -> int:
+        """Device address of p's staged kernel arguments (moss_adam_params + encode scale)."""
+        return self.hp_dev.data_ptr() + self.index[id(p)] * self._WORDS * 4
 
     def zero_grad(self, set_to_none: bool = True) -> None:
         for p in self.params:
@@ -365,6 +379,8 @@ class MossAdamW:
         base = self.hp_dev.data_ptr()
         stride = self._WORDS * 4
         for i, p in enumerate(self.params):
+            if id(p) in self.sharded:
+                continue
             layer = getattr(p, "moss_layer", None)
             g = p.main_grad if layer is not None else p.grad
             if g is None:
@@ -390,7 +406,7 @@ class MossAdamW:
         """JIT snap of every MOSS scale to max|W'|/448 and re-encode (autoscale.py:86-96)."""
         for p in self.params:
             layer = getattr(p, "moss_layer", None)
-            if layer is None:
+            if layer is None or id(p) in self.sharded:
                 continue
             sched = layer.schedule
             amax = float(layer.w_amax.item())

@@ -44,6 +44,8 @@ def train(model: LlamaModel, data: MarkovTokens, *, steps: int, batch: int, seq:
     """``cuda_graph=True`` (single GPU) captures forward + backward + the
     optimizer kernels once and replays the graph each step (nn.CudaGraphStep)."""
     opt = make_optimizer(model, lr, steps, warmup, weight_decay)
+    if callable(buckets):                            # a factory: e.g. lambda opt: Zero1(opt)
+        buckets = buckets(opt)
     if buckets is not None:
         opt.grad_scale = buckets.grad_scale
     dev = next(model.parameters()).device
@@ -75,7 +77,10 @@ def train(model: LlamaModel, data: MarkovTokens, *, steps: int, batch: int, seq:
             loss.backward()
             if buckets is not None:
                 buckets.finish()
-            opt.step()
+            if hasattr(buckets, "step"):
+                buckets.step()                       # zero.Zero1: sharded update + FP8 all-gather
+            else:
+                opt.step()
         lv = float(loss.detach())
         if step % check_every == 0:
             opt.check(f"step {step}")
