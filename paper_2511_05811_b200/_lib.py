@@ -60,6 +60,15 @@ def lib() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("MOSS_B200_LIB", LIB)     # override: debug builds (tools/gemm_timeline.py)
+    if path != LIB:
+        handle = ctypes.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+        return _lib
     if not os.path.exists(LIB):
         from .build import build
         try:
