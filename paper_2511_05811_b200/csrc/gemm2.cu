@@ -209,22 +209,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
             const uint64_t bdesc0 = umma_desc(smem_u32(s_b), 0, 1024, kLayoutSW128);
             const uint64_t sfadesc0 = umma_desc(smem_u32(s_sfa), 0, 128, kLayoutNone);
             const uint64_t sfbdesc0 = umma_desc(smem_u32(s_sfb), 0, 128, kLayoutNone);
+            auto copy_sf = [&](uint32_t sa, uint32_t sb) {
+                tmem_cp_sf_2cta(sa, sfadesc0 + (uint64_t)((stage * L::SFA_BYTES) >> 4));
+                if (!unit_b) {
+#pragma unroll
+                    for (int j = 0; j < G2_BN / 128; ++j)
+                        tmem_cp_sf_2cta(sb + j * 4, sfbdesc0 + (uint64_t)((stage * L::SFB_BYTES + j * 512) >> 4));
+                }
+            };
             int it_ = 0;
             for (int tile = pair; tile < num_tiles; tile += npairs, ++it_) {
+                // The first k-block's scale factors go into TMEM BEFORE the accumulator
+                // is released: the SF columns are separate and double-buffered, and
+                // tcgen05 ops of this thread execute in issue order, so the copy cannot
+                // overtake the previous tile's MMAs.  Takes the copies off the handoff.
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (elect_one()) copy_sf(tm_sfa + sfbuf, tm_sfb + sfbuf);
+                __syncwarp();
                 mbar_wait(tmem_empty, acc_phase ^ 1);
                 tc_fence_after();
                 if (lane == 0) G2_STAMP(pair, it_, 0);
                 for (int kb = 0; kb < kblocks; ++kb) {
-                    mbar_wait(&full[stage], phase);
-                    tc_fence_after();
+                    if (kb > 0) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                    }
                     if (elect_one()) {
                         const uint32_t sa = tm_sfa + sfbuf, sb = tm_sfb + sfbuf;
-                        tmem_cp_sf_2cta(sa, sfadesc0 + (uint64_t)((stage * L::SFA_BYTES) >> 4));
-                        if (!unit_b) {
-#pragma unroll
-                            for (int j = 0; j < G2_BN / 128; ++j)
-                                tmem_cp_sf_2cta(sb + j * 4, sfbdesc0 + (uint64_t)((stage * L::SFB_BYTES + j * 512) >> 4));
-                        }
+                        if (kb > 0) copy_sf(sa, sb);
                         const uint64_t adesc = adesc0 + (uint64_t)((stage * L::A_BYTES) >> 4);
                         const uint64_t bdesc = bdesc0 + (uint64_t)((stage * L::B_BYTES) >> 4);
 #pragma unroll
