@@ -150,6 +150,68 @@ __global__ void __launch_bounds__(NT, (1024 / NT > 0 ? 1024 / NT : 1)) rmsnorm_f
     block_amax_commit(m, red_u, amax);
 }
 
+// The same forward with ONE WARP PER ROW (d = 256 * VPL, VPL <= 16): no block
+// barriers, the whole row (and delta) in flight per warp — 16 KB per warp,
+// 128 KB per SM — instead of one 8 KB row per 512-thread CTA between two
+// __syncthreads.  Used for d % 256 == 0 (every Llama width here).
+template <int VPL>
+__global__ void __launch_bounds__(256) rmsnorm_fwd_warp_kernel(const __nv_bfloat16* __restrict__ x,
+                                                               const __nv_bfloat16* __restrict__ delta,
+                                                               __nv_bfloat16* __restrict__ x_out,
+                                                               const float* __restrict__ w, float eps,
+                                                               __nv_bfloat16* __restrict__ y, float* __restrict__ rstd,
+                                                               uint32_t* amax, int T, int d) {
+    __shared__ uint32_t red_u[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t m = 0;
+    for (int t = blockIdx.x * 8 + warp; t < T; t += gridDim.x * 8) {
+        const int64_t row = (int64_t)t * d;
+        uint4 v[VPL];
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) v[i] = *reinterpret_cast<const uint4*>(x + row + (i * 32 + lane) * 8);
+        if (delta) {
+#pragma unroll
+            for (int i = 0; i < VPL; ++i) {
+                const uint4 dd = *reinterpret_cast<const uint4*>(delta + row + (i * 32 + lane) * 8);
+                float a[8], b[8];
+                unpack_bf16x8(v[i], a);
+                unpack_bf16x8(dd, b);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) a[j] += b[j];
+                v[i] = bf16x8_pack(a);
+                *reinterpret_cast<uint4*>(x_out + row + (i * 32 + lane) * 8) = v[i];
+            }
+        }
+        float ss = 0.f;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+            float a[8];
+            unpack_bf16x8(v[i], a);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ss = fmaf(a[j], a[j], ss);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xFFFFFFFFu, ss, o);
+        const float r = rsqrtf(ss / (float)d + eps);
+        if (lane == 0) rstd[t] = r;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+            const int c = (i * 32 + lane) * 8;
+            const float4 w0 = __ldg(reinterpret_cast<const float4*>(w + c));
+            const float4 w1 = __ldg(reinterpret_cast<const float4*>(w + c + 4));
+            const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            float a[8];
+            unpack_bf16x8(v[i], a);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a[j] = a[j] * r * wv[j];
+            const uint4 ob = bf16x8_pack(a);
+            *reinterpret_cast<uint4*>(y + row + c) = ob;
+            m = max(m, absmax_bits_bf16(ob));
+        }
+    }
+    block_amax_commit(m, red_u, amax);
+}
+
 // backward: xh = f32(x') * rstd; gw = f32(dy) * w; c = mean(gw * xh)
 //   dx = bf16( rstd * (gw - xh * c) + f32(d_res) )   (d_res: gradient arriving
 //        through the residual stream; null = 0)
@@ -402,6 +464,26 @@ static int amax_reset(uint32_t* amax, cudaStream_t st) {
 int launch_rmsnorm_fwd(const void* x, const void* delta, void* x_out, const float* w, float eps, void* y, float* rstd,
                        float* amax, int64_t T, int64_t d, cudaStream_t st) {
     if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
+    if (d % 256 == 0 && d / 256 <= 16) {
+        auto warp_args = [&](auto kern) {
+            static int occ = resident(kern, 256);
+            const int grid = (int)std::min<int64_t>((T + 7) / 8, (int64_t)sm_count() * occ);
+            kern<<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)delta, (__nv_bfloat16*)x_out, w,
+                                       eps, (__nv_bfloat16*)y, rstd, reinterpret_cast<uint32_t*>(amax), (int)T, (int)d);
+        };
+        switch (d / 256) {
+            case 1: warp_args(rmsnorm_fwd_warp_kernel<1>); break;
+            case 2: warp_args(rmsnorm_fwd_warp_kernel<2>); break;
+            case 3: warp_args(rmsnorm_fwd_warp_kernel<3>); break;
+            case 4: warp_args(rmsnorm_fwd_warp_kernel<4>); break;
+            case 8: warp_args(rmsnorm_fwd_warp_kernel<8>); break;
+            case 12: warp_args(rmsnorm_fwd_warp_kernel<12>); break;
+            case 16: warp_args(rmsnorm_fwd_warp_kernel<16>); break;
+            default: goto block_path;
+        }
+        return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+    }
+block_path:
     const int nt = (int)((d / 8 + 31) / 32 * 32);
     auto args = [&](auto kern) {
         static int occ = resident(kern, nt);     // one static per template instance
