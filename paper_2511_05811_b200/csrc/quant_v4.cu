@@ -88,6 +88,9 @@ struct Q4Global {
     uint32_t gbits;
     float rg;        // RN(1/g) (valid when g_normal)
     bool g_normal;
+    bool fast;       // g normal and in [2^-60, 2^60): the block fast path applies
+    int emin;        // fast path needs e in [emin, emax]: eff = g 2^e in [2^-60, 2^60), e in [-127, 127]
+    uint32_t erange; // emax - emin
 };
 
 __device__ __forceinline__ Q4Global q4_global(float amax) {
@@ -96,6 +99,10 @@ __device__ __forceinline__ Q4Global q4_global(float amax) {
     G.gbits = __float_as_uint(G.g);
     G.g_normal = G.gbits >= 0x00800000u;
     G.rg = __frcp_rn(G.g);
+    const int eg = (int)(G.gbits >> 23);
+    G.fast = G.g_normal && eg >= 67 && eg <= 186;
+    G.emin = max(67 - eg, -127);
+    G.erange = (uint32_t)(min(186 - eg, 127) - G.emin);
     return G;
 }
 
@@ -158,6 +165,44 @@ __device__ __forceinline__ void q4_encode(const float (&lo)[NP], const float (&h
             out[q] = e4m3x4(__fdiv_rn(-lo[2 * q], eff), __fdiv_rn(-hi[2 * q], eff), __fdiv_rn(-lo[2 * q + 1], eff),
                             __fdiv_rn(-hi[2 * q + 1], eff));
     }
+}
+
+// One 32-element block (16 packed bf16 pairs): unpack, max, E8M0 code, codes.
+// Fast path (every block of real data): branch-free scale math —
+//   e = ceil(log2(s/g)) = (bits(s) - bits(g) + 0x7FFFFF) >> 23,
+//   eff = g 2^e and r = RN(1/g) 2^-e as integer exponent adds (one IMAD each) —
+// taken when the whole warp's blocks satisfy bm in {0} u [2^-100, inf) and
+// eff = g 2^e in [2^-60, 2^60) (then every value above is exact and equal to
+// the general path: see the header).  Otherwise the warp runs q4_scale +
+// q4_encode, the general path (one vote per block, no per-thread divergence).
+template <int NP>
+__device__ __forceinline__ uint32_t q4_block(const uint32_t (&w)[NP], const Q4Global& G, bool& rerr,
+                                             uint32_t (&out)[NP / 2]) {
+    float lo[NP], hi[NP];
+    const float bm = q4_unpack(w, lo, hi);
+    const float s = div1(bm, -kE4M3Max, 0x1.24924ap-9f);
+    int e = ((int)(__float_as_uint(s) - G.gbits) + 0x7FFFFF) >> 23;
+    e = bm > 0.f ? e : 0;
+    const bool tiny = (__float_as_uint(bm) - 1u) < (0x0D800000u - 1u);          // 0 < bm < 2^-100
+    const bool slow = !G.fast || tiny || (uint32_t)(e - G.emin) > G.erange;
+    if (__any_sync(0xFFFFFFFFu, slow)) {
+        int e2;
+        float eff2;
+        const uint32_t code = q4_scale(bm, G, rerr, e2, eff2);
+        q4_encode(lo, hi, e2, eff2, G, out);
+        return code;
+    }
+    const float eff = __uint_as_float(G.gbits + (uint32_t)e * 0x00800000u);
+    const float r = __uint_as_float(__float_as_uint(G.rg) - (uint32_t)e * 0x00800000u);
+    const uint64_t nr2 = pk(-r, -r), b2 = pk(eff, eff);
+#pragma unroll
+    for (int q = 0; q < NP / 2; ++q) {
+        float a0, a1, b0, b1;
+        upk(div2n(pk(lo[2 * q], hi[2 * q]), b2, nr2), a0, a1);
+        upk(div2n(pk(lo[2 * q + 1], hi[2 * q + 1]), b2, nr2), b0, b1);
+        out[q] = e4m3x4(a0, a1, b0, b1);
+    }
+    return (uint32_t)(e + 127);
 }
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
@@ -284,15 +329,31 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
     // col pass: thread (rb, cp) owns the 32-row blocks rb of columns 2cp, 2cp+1.
     // (A 512-thread variant with half-blocks per thread measured 25 % slower:
     // the kernel is ALU-issue bound and the split adds per-block work.)
+    // All smem offsets are hoisted out of the tile loop: with the SWIZZLE_128B
+    // layouts the per-access offset is a per-thread base XOR a compile-time
+    // chunk index (the base has zero bits 4-6).
     bool rerr = false;
     const int rr = tid & 127, kb0 = tid >> 7;
     const int rb = tid >> 6, cp = tid & 63;
-    uint32_t cbase[8];   // col-pass smem offset of row rb*32 + i, column 2cp: cbase[i & 7] + i*128
+    // row-pass loads: block kb0 + 2h, 16 B chunk q: rbase ^ (q << 4) + h * 16384
+    const uint32_t rbase = (uint32_t)(rr * 128 + ((((kb0 * 4) ^ (rr & 7)) & 7) << 4));
+    // row-pass stores: code bytes (kb0 + 2h)*32 + 16j: obase ^ ((4h + j) << 4)
+    const uint32_t obase = (uint32_t)(rr * 128 + ((((kb0 * 2) ^ (rr & 7)) & 7) << 4));
+    const int sfo_row = ((rr & 31) << 4) + ((rr >> 5) << 2) + kb0;        // + 2h
+    uint32_t cbase[8];   // col-pass loads: row rb*32 + i, column 2cp -> cbase[i & 7] + i*128
     {
         const int c = 2 * cp;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             cbase[k] = (uint32_t)((c >> 6) * 16384 + rb * 32 * 128 + ((((c >> 3) & 7) ^ k) << 4) + ((c & 7) << 1));
+    }
+    uint32_t cob[2];     // col-pass stores: output row c = 2cp + h, bytes rb*32 + 16j: cob[h] ^ (j << 4)
+    int sfo_col[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int c = 2 * cp + h;
+        cob[h] = (uint32_t)(c * 128 + ((((rb * 2) ^ (c & 7)) & 7) << 4));
+        sfo_col[h] = 512 + ((c & 31) << 4) + ((c >> 5) << 2) + rb;
     }
     for (int p = 0; p < n; ++p) {
         const int j = desc ? n - 1 - p : p;
@@ -312,31 +373,24 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
         if (ROW) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int kb = kb0 + 2 * h;
                 uint32_t w[16];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const uint4 u = *reinterpret_cast<const uint4*>(T + q4_in_off(rr, kb * 32 + q * 8));
+                    const uint4 u = *reinterpret_cast<const uint4*>(T + h * 16384 + (rbase ^ (uint32_t)(q << 4)));
                     w[4 * q] = u.x; w[4 * q + 1] = u.y; w[4 * q + 2] = u.z; w[4 * q + 3] = u.w;
                 }
-                float lo[16], hi[16];
-                const float bm = q4_unpack(w, lo, hi);
-                int e;
-                float eff;
-                const uint32_t code = q4_scale(bm, Gs, rerr, e, eff);
-                q4_encode(lo, hi, e, eff, Gs, rcodes[h]);
-                sfs[q4_sf_in_chunk(rr, kb)] = (uint8_t)code;
-                if (MICRO && micro) micro[(int64_t)(r0 + rr) * (cols >> 5) + (c0 >> 5) + kb] = (uint8_t)code;
+                const uint32_t code = q4_block(w, Gs, rerr, rcodes[h]);
+                sfs[sfo_row + 2 * h] = (uint8_t)code;
+                if (MICRO && micro) micro[(int64_t)(r0 + rr) * (cols >> 5) + (c0 >> 5) + kb0 + 2 * h] = (uint8_t)code;
             }
         }
         __syncthreads();                           // the whole tile is in registers: reuse the slot for codes
         if (ROW) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int kb = kb0 + 2 * h;
-                *reinterpret_cast<uint4*>(T + q4_out_off(rr, kb * 32)) =
+                *reinterpret_cast<uint4*>(T + (obase ^ (uint32_t)((4 * h) << 4))) =
                     make_uint4(rcodes[h][0], rcodes[h][1], rcodes[h][2], rcodes[h][3]);
-                *reinterpret_cast<uint4*>(T + q4_out_off(rr, kb * 32 + 16)) =
+                *reinterpret_cast<uint4*>(T + (obase ^ (uint32_t)((4 * h + 1) << 4))) =
                     make_uint4(rcodes[h][4], rcodes[h][5], rcodes[h][6], rcodes[h][7]);
             }
         }
@@ -350,18 +404,13 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
                 for (int i = 0; i < 16; ++i)
                     w[i] = h ? __byte_perm(ucol[2 * i], ucol[2 * i + 1], 0x7632)
                              : __byte_perm(ucol[2 * i], ucol[2 * i + 1], 0x5410);
-                float lo[16], hi[16];
-                const float bm = q4_unpack(w, lo, hi);
-                int e;
-                float eff;
-                const uint32_t code = q4_scale(bm, Gs, rerr, e, eff);
                 uint32_t cc[8];
-                q4_encode(lo, hi, e, eff, Gs, cc);
-                const int c = 2 * cp + h;
-                *reinterpret_cast<uint4*>(Tc + q4_out_off(c, rb * 32)) = make_uint4(cc[0], cc[1], cc[2], cc[3]);
-                *reinterpret_cast<uint4*>(Tc + q4_out_off(c, rb * 32 + 16)) = make_uint4(cc[4], cc[5], cc[6], cc[7]);
-                sfs[512 + q4_sf_in_chunk(c, rb)] = (uint8_t)code;
-                if (MICRO && micro_t) micro_t[(int64_t)(c0 + c) * (rows >> 5) + (r0 >> 5) + rb] = (uint8_t)code;
+                const uint32_t code = q4_block(w, Gs, rerr, cc);
+                *reinterpret_cast<uint4*>(Tc + cob[h]) = make_uint4(cc[0], cc[1], cc[2], cc[3]);
+                *reinterpret_cast<uint4*>(Tc + (cob[h] ^ 16u)) = make_uint4(cc[4], cc[5], cc[6], cc[7]);
+                sfs[sfo_col[h]] = (uint8_t)code;
+                if (MICRO && micro_t)
+                    micro_t[(int64_t)(c0 + 2 * cp + h) * (rows >> 5) + (r0 >> 5) + rb] = (uint8_t)code;
             }
         }
         fence_proxy_async_smem();
