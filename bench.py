@@ -181,6 +181,47 @@ def gemm_vs_cublas(dev, tokens: int) -> dict | None:
                    "10 back-to-back launches each, CUDA events; cuBLASLt via torch F.scaled_mm" % tokens}
 
 
+def quantizer_rates(dev, tokens: int, hbm: float) -> dict:
+    """K1 on the 8 tensors one layer step quantizes (inputs and output-gradients
+    of the four linears, row + column-wise), both modes: the single launch with
+    the in-kernel amax (input read twice when it exceeds smem + L2) and the
+    producer-amax mode the Llama decoder runs (input read once).  GB/s of
+    ALGORITHMIC bytes (4.063 B/elem), back-to-back launches."""
+    import torch
+
+    from paper_2511_05811_b200 import _lib
+    from paper_2511_05811_b200.quantize import sf_buffer
+    fl = _lib.FlagWord(dev)
+    res = {}
+    for mode in ("single_launch_amax", "producer_amax"):
+        byts = ms = 0.0
+        for cols in (4096, 4096, 4096, 11008, 12288, 4096, 22016, 4096):
+            x = torch.randn(tokens, cols, device=dev, dtype=torch.bfloat16)
+            am = x.float().abs().max().reshape(1)
+            c = torch.empty(tokens, cols, dtype=torch.uint8, device=dev)
+            ct = torch.empty(cols, tokens, dtype=torch.uint8, device=dev)
+            sf, sft = sf_buffer(tokens, cols, dev), sf_buffer(cols, tokens, dev)
+            g = torch.empty(1, device=dev)
+            fn = lambda: _lib.quant_mx2_fused(x, am, fl, amax_given=mode == "producer_amax", codes=c, sf=sf,
+                                               codes_t=ct, sf_t=sft, g_out=g)
+            for _ in range(3):
+                fn()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for _ in range(10):
+                fn()
+            e.record()
+            torch.cuda.synchronize()
+            ms += s.elapsed_time(e) / 10
+            byts += tokens * cols * (4 + 2 / 32)
+        res[mode] = {"achieved_gbs": byts / (ms / 1e3) / 1e9, "frac_of_hbm": byts / (ms / 1e3) / 1e9 / hbm,
+                     "ms_per_step": ms}
+    fl.raise_if_set("quantizer_rates")
+    res["how"] = ("the 8 row+col quantizations of one layer step at M=%d, 10 back-to-back launches each (inputs > "
+                  "L2 are re-read by the single-launch mode), algorithmic bytes 4.063 B/elem" % tokens)
+    return res
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """SM clock and throttle reasons sampled DURING the timed region (NVML in a
@@ -503,6 +544,10 @@ def main() -> None:
             cmp = {"error": str(ex)[:200]}
         if cmp:
             line["roofline"]["library_reference"] = cmp
+        try:
+            line["kernels"]["quantize_standalone"] = quantizer_rates(dev, T, hbm)
+        except Exception as ex:  # noqa: BLE001
+            line["kernels"]["quantize_standalone"] = {"error": str(ex)[:200]}
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_sample(1024, 4096)
         line["cpu_baseline"].pop("seconds", None)
