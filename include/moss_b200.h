@@ -187,6 +187,19 @@ int moss_rope_bwd(const void* dq, const void* dk, const void* dv, const float* c
  * (per-tensor codes commute with the transpose).  rows, cols % 16 == 0. */
 int moss_transpose_u8(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Per-group (COAT-style) comparator — NOT the MOSS path; the ablation the
+ * paper contrasts MOSS with (Fig. 1 / Table 7).
+ * quant_per_group (quantize.py:100-124), group = 128 along rows:
+ *   scales [rows, cols/128] f32 = f32(amax/448) (0 -> 1), codes = e4m3(x / s) */
+int moss_quant_per_group(const void* x, int dtype, int64_t rows, int64_t cols, int64_t group, uint8_t* codes,
+                         float* scales, uint32_t* flags, void* stream);
+/* gemm_pergroup_mainloop (gemm.py:132-157): D = sum_g (A_g B_g^T) sa[:, g] sb[:, g]^T,
+ * every 128-deep partial product rescaled on the CUDA cores ("promotion").
+ * Scales GROUP-MAJOR: sa_t [K/128, M], sb_t [K/128, N] f32.  M, N, K % 128 == 0. */
+int moss_gemm_pergroup(const uint8_t* A, const float* sa_t, const uint8_t* B, const float* sb_t, void* D,
+                       int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, void* stream);
+
 /* Human-readable status. */
 const char* moss_strerror(int status);
 

@@ -45,6 +45,8 @@ _SIGS = {
     "moss_rope_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
     "moss_rope_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
     "moss_transpose_u8": (_I, [_P, _P, _I64, _I64, _P]),
+    "moss_quant_per_group": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P, _P]),
+    "moss_gemm_pergroup": (_I, [_P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _P]),
     "moss_encode_scaled": (_I, [_P, _I, _I64, _I64, _P, _F, _I, _P, _P, _P, _P, _P, _P]),
     "moss_gemm_mxf8": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _I, _P]),
     "moss_adamw_fp8": (_I, [_P, _P, _I, _P, _P, _I64, _I64, ctypes.POINTER(AdamParams), _F, _P, _P, _P,
@@ -345,3 +347,18 @@ def transpose_u8(src: torch.Tensor, dst: torch.Tensor) -> None:
     rows, cols = src.shape
     with _Span("transpose", 2 * rows * cols):
         check(lib().moss_transpose_u8(src.data_ptr(), dst.data_ptr(), rows, cols, stream()), "moss_transpose_u8")
+
+
+def quant_per_group(x2d, codes, scales, flags: FlagWord, group: int = 128) -> None:
+    rows, cols = x2d.shape
+    with _Span("quant_pg", rows * cols * (x2d.element_size() + 1)):
+        check(lib().moss_quant_per_group(x2d.data_ptr(), dtype_code(x2d), rows, cols, group, codes.data_ptr(),
+                                         scales.data_ptr(), flags.ptr, stream()), "moss_quant_per_group")
+
+
+def gemm_pergroup(a, sa_t, b, sb_t, d) -> None:
+    m, k = a.shape
+    n = b.shape[0]
+    with _Span("gemm_pg", 2.0 * m * n * k):
+        check(lib().moss_gemm_pergroup(a.data_ptr(), sa_t.data_ptr(), b.data_ptr(), sb_t.data_ptr(), d.data_ptr(),
+                                       dtype_code(d), d.stride(0), m, n, k, stream()), "moss_gemm_pergroup")

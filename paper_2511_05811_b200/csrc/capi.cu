@@ -35,6 +35,10 @@ int launch_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void*
 int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
                     float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, cudaStream_t st);
 int launch_transpose_u8(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t st);
+int launch_quant_per_group(const void* x, int dtype, int64_t rows, int64_t cols, uint8_t* codes, float* scales,
+                           uint32_t* flags, cudaStream_t st);
+int launch_gemm_pergroup(const uint8_t* A, const float* sa_t, const uint8_t* B, const float* sb_t, void* D,
+                         int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, cudaStream_t st);
 }  // namespace moss
 
 static inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
@@ -216,6 +220,27 @@ int moss_transpose_u8(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t co
     if (!src || !dst) return MOSS_ERR_ARGUMENT;
     if (!aligned(src, 16) || !aligned(dst, 16) || cols % 16 || rows % 16) return MOSS_ERR_ALIGN;
     return moss::launch_transpose_u8(src, dst, rows, cols, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------- per-group comparator (COAT-style)
+int moss_quant_per_group(const void* x, int dtype, int64_t rows, int64_t cols, int64_t group, uint8_t* codes,
+                         float* scales, uint32_t* flags, void* stream) {
+    if (rows <= 0 || cols <= 0) return MOSS_ERR_SHAPE;
+    if (group != 128) return MOSS_ERR_ARGUMENT;             /* the comparator's group size */
+    if (cols % 128) return MOSS_ERR_SHAPE;
+    if (!x || !codes || !scales || !flags || !dtype_ok(dtype)) return MOSS_ERR_ARGUMENT;
+    if (!aligned(x, 16) || !aligned(codes, 4) || !aligned(scales, 4)) return MOSS_ERR_ALIGN;
+    return moss::launch_quant_per_group(x, dtype, rows, cols, codes, scales, flags, (cudaStream_t)stream);
+}
+
+int moss_gemm_pergroup(const uint8_t* A, const float* sa_t, const uint8_t* B, const float* sb_t, void* D,
+                       int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, void* stream) {
+    if (M <= 0 || N <= 0 || K <= 0 || M % 128 || N % 128 || K % 128) return MOSS_ERR_SHAPE;
+    if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX || ldd < N) return MOSS_ERR_SHAPE;
+    if (!A || !B || !sa_t || !sb_t || !D || !dtype_ok(d_dtype)) return MOSS_ERR_ARGUMENT;
+    if (!aligned(A, 16) || !aligned(B, 16) || !aligned(sa_t, 16) || !aligned(sb_t, 16) || !aligned(D, 16) || ldd % 8)
+        return MOSS_ERR_ALIGN;
+    return moss::launch_gemm_pergroup(A, sa_t, B, sb_t, D, d_dtype, ldd, M, N, K, (cudaStream_t)stream);
 }
 
 }  // extern "C"

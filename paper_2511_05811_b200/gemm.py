@@ -44,6 +44,36 @@ def mx_epilogue_counters(m: int, n: int, k: int, k2: int = 32) -> GemmCounters:
     return GemmCounters(0, m * n, m * n * (k // k2), m * n * k)
 
 
+def pergroup_mainloop_counters(m: int, n: int, k: int, group_size: int = 128) -> GemmCounters:
+    """Closed-form cost counts of the main-loop dataflow (gemm.py:67-74)."""
+    if k % group_size != 0:
+        raise InvalidShapeError(f"K={k} not divisible by group size {group_size}")
+    return GemmCounters(m * n * (k // group_size), 0, 0, m * n * k)
+
+
+def gemm_pergroup_mainloop(qa, qb) -> tuple[torch.Tensor, GemmCounters]:
+    """C = sum_g (A_g B_g^T) * sa_g sb_g^T with every 128-deep partial product
+    rescaled in the K loop (gemm.py:132-157) — the COAT-style comparator on
+    tcgen05 (kind::f8f6f4, no block scale) + CUDA-core promotion
+    (csrc/pergroup.cu).  Returns (C float32 [M, N] on the GPU, counters)."""
+    if qa.codes.dim() != 2 or qb.codes.dim() != 2:
+        raise InvalidShapeError("gemm operands must be 2-D")
+    if qa.codes.shape[1] != qb.codes.shape[1]:
+        raise InvalidShapeError(f"K mismatch: {tuple(qa.codes.shape)} vs {tuple(qb.codes.shape)}")
+    if qa.group_size != qb.group_size:
+        raise InvalidArgumentError("operands must share one group size")
+    m, k = qa.codes.shape
+    n = qb.codes.shape[0]
+    group = qa.group_size
+    if k % group != 0:
+        raise InvalidShapeError(f"K={k} not divisible by group size {group}")
+    if m % 128 or n % 128:
+        raise InvalidShapeError("the per-group comparator covers M, N multiples of 128")
+    d = torch.empty((m, n), dtype=torch.float32, device=qa.codes.device)
+    _lib.gemm_pergroup(qa.codes, qa.scales.t().contiguous(), qb.codes, qb.scales.t().contiguous(), d)
+    return d, pergroup_mainloop_counters(m, n, k, group)
+
+
 @dataclass(frozen=True)
 class GemmOperands:
     """Quantized W (M, K) per-tensor and X (N, K) two-level (gemm.py:77-105)."""

@@ -28,8 +28,8 @@ from . import _lib
 from .errors import InvalidArgumentError, InvalidShapeError
 from .fp8 import E4M3, E8m0Rounding, Fp8Format, e8m0_decode, fp8_decode
 
-__all__ = ["PerTensorQuant", "TwoLevelQuant", "quant_per_tensor", "quant_two_level", "dequantize",
-           "MX2Operand", "quantize_mx2", "sf_buffer"]
+__all__ = ["PerTensorQuant", "TwoLevelQuant", "PerGroupQuant", "quant_per_tensor", "quant_two_level",
+           "quant_per_group", "dequantize", "MX2Operand", "quantize_mx2", "sf_buffer"]
 
 
 @dataclass(frozen=True)
@@ -63,6 +63,43 @@ class TwoLevelQuant:
 
     def micro_scales(self) -> torch.Tensor:
         return e8m0_decode(self.micro_codes)
+
+
+@dataclass(frozen=True)
+class PerGroupQuant:
+    """quant_per_group result (quantize.py:54-62): the COAT-style comparator, not the MOSS path."""
+    codes: torch.Tensor     # uint8, source shape
+    scales: torch.Tensor    # float32, outer shape + (n_groups,)
+    group_size: int
+    fmt: Fp8Format
+
+    @property
+    def shape(self):
+        return tuple(self.codes.shape)
+
+
+def quant_per_group(x, fmt: Fp8Format = E4M3, group_size: int = 128) -> PerGroupQuant:
+    """One f32 scale per contiguous group of ``group_size`` along the last axis
+    (quantize.py:100-124) on the GPU (csrc/pergroup.cu).  The ablation
+    comparator of the paper's per-group (COAT) contrast; group_size 128, the
+    last dim a multiple of 128 (the reference's ragged final group is not on
+    the comparator's shapes)."""
+    if group_size < 1:
+        raise InvalidArgumentError(f"group_size must be >= 1, got {group_size}")
+    if fmt != E4M3 or group_size != 128:
+        raise InvalidArgumentError("the GPU per-group comparator covers E4M3, group_size=128")
+    xf = _to_device_2d(x)
+    rows, cols = xf.shape
+    if cols % 128:
+        raise InvalidShapeError(f"last dim {cols} not a multiple of the group size 128")
+    codes = torch.empty((rows, cols), dtype=torch.uint8, device=xf.device)
+    scales = torch.empty((rows, cols // 128), dtype=torch.float32, device=xf.device)
+    fl = _lib.FlagWord(xf.device)
+    _lib.quant_per_group(xf, codes, scales, fl)
+    fl.raise_if_set("quant_per_group")
+    shp = tuple(x.shape) if hasattr(x, "shape") else xf.shape
+    return PerGroupQuant(codes=codes.view(shp), scales=scales.view(tuple(shp[:-1]) + (cols // 128,)),
+                         group_size=group_size, fmt=fmt)
 
 
 def sf_buffer(rows: int, cols: int, device) -> torch.Tensor:
