@@ -7,12 +7,13 @@ the GEMM running on the B200 kernels.
     python -m paper_2511_05811_b200.cli gemm --m 256 --n 512 --k 1024 --scheme mx2 --verify --out r.json
     python -m paper_2511_05811_b200.cli codec-table --format e4m3
 
-Covered: ``quantize`` (schemes ``tensor`` and ``mx2``, E4M3, CEIL_POW2, k2=32:
-cli.py:93-133), ``gemm`` (scheme ``mx2``, counters or ``--verify`` against the
-float64 dequantize-then-multiply oracle: cli.py:221-275), ``codec-table``
-(cli.py:71-90).  The per-group scheme, E5M2, NEAREST_LOG2, the SNR / bound /
-autoscale / train simulations are not on the MOSS hot path and exit with the
-reference's error convention.  Errors print a JSON line
+Covered: ``quantize`` (schemes ``tensor``, ``mx2`` and — through the COAT
+comparator — ``group`` with group size 128; E4M3, CEIL_POW2, k2=32:
+cli.py:93-133), ``gemm`` (schemes ``mx2`` and ``pergroup``, counters or
+``--verify`` against the float64 dequantize-then-multiply oracle:
+cli.py:221-275), ``codec-table`` (cli.py:71-90).  E5M2, NEAREST_LOG2, other
+group sizes and the SNR / bound / autoscale / train simulations are not on the
+MOSS hot path and exit with the reference's error convention.  Errors print a JSON line
 ``{"error": <class>, "message": ...}`` and exit 1 (cli.py:313-315).
 """
 
@@ -88,9 +89,9 @@ def codec_table(fmt_name, out):
 @click.option("--rounding", type=click.Choice(["ceil", "nearest"]), default="ceil")
 def quantize(scheme, fmt_name, in_path, out, meta, group_size, k2, rounding):
     """Quantize a .mosst f32 tensor on the GPU and write codes + metadata (cli.py:93-133)."""
-    from .quantize import quant_per_tensor, quant_two_level
-    if scheme == "group":
-        _unsupported("the per-group scheme")
+    from .quantize import quant_per_group, quant_per_tensor, quant_two_level
+    if scheme == "group" and group_size != 128:
+        _unsupported("per-group sizes other than 128")
     if fmt_name != "e4m3":
         _unsupported("E5M2")
     if rounding != "ceil" or k2 != 32:
@@ -103,6 +104,11 @@ def quantize(scheme, fmt_name, in_path, out, meta, group_size, k2, rounding):
     if scheme == "tensor":
         q = quant_per_tensor(x, E4M3)
         doc["scale"] = float(q.scale)
+    elif scheme == "group":
+        q = quant_per_group(x, E4M3, group_size=group_size)
+        doc["group_size"] = group_size
+        doc["scales"] = [float(v) for v in q.scales.cpu().numpy().ravel()]
+        doc["scales_shape"] = list(q.scales.shape)
     else:
         q = quant_two_level(x, E4M3)
         micro_path = str(out) + ".micro.mosst"
@@ -137,14 +143,28 @@ def gemm(m, n, k, scheme, verify, show_counters, seed, out):
     import torch
 
     from .fp8 import fp8_decode
-    from .gemm import gemm_mx_epilogue, mx_epilogue_counters, quantize_gemm_operands
-    if scheme == "pergroup":
-        _unsupported("the per-group (COAT) GEMM")
-    if k % 32 != 0:
+    from .gemm import (gemm_mx_epilogue, gemm_pergroup_mainloop, mx_epilogue_counters, pergroup_mainloop_counters,
+                       quantize_gemm_operands)
+    from .quantize import quant_per_group
+    if scheme == "mx2" and k % 32 != 0:
         raise click.ClickException("mx2 requires K divisible by 32")
+    if scheme == "pergroup" and k % 128 != 0:
+        raise click.ClickException("pergroup requires K divisible by 128")
     report = {"m": m, "n": n, "k": k, "scheme": scheme, "seed": seed}
-    ctr = mx_epilogue_counters(m, n, k)
-    if verify:
+    ctr = mx_epilogue_counters(m, n, k) if scheme == "mx2" else pergroup_mainloop_counters(m, n, k)
+    if verify and scheme == "pergroup":
+        # the COAT-style comparator (csrc/pergroup.cu); checker: float64 product of the dequantized groups
+        qa = quant_per_group(tensor_randn([m, k], seed=seed))
+        qb = quant_per_group(tensor_randn([n, k], seed=seed + 1))
+        outm, ctr = gemm_pergroup_mainloop(qa, qb)
+        deq = lambda q, r: (fp8_decode(q.codes).double().view(r, k // 128, 128)
+                            * q.scales.double()[..., None]).view(r, k)
+        oracle = deq(qa, m) @ deq(qb, n).t()
+        diff = outm.double() - oracle
+        denom = float(torch.linalg.norm(oracle))
+        report["max_rel_error"] = float((diff.abs() / oracle.abs().clamp_min(1e-30)).max())
+        report["frobenius_rel_error"] = float(torch.linalg.norm(diff)) / denom if denom else 0.0
+    elif verify:
         w = tensor_randn([m, k], seed=seed)
         x = tensor_randn([n, k], seed=seed + 1)
         ops = quantize_gemm_operands(w, x)

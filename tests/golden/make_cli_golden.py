@@ -10,7 +10,9 @@ writes:
   tests/golden/cli/ref_mx2*        `mossq quantize --scheme mx2` outputs
                                    (codes .mosst, micro .mosst, meta JSON)
   tests/golden/cli/ref_tensor*     `mossq quantize --scheme tensor` outputs
+  tests/golden/cli/ref_group*      `mossq quantize --scheme group` outputs
   tests/golden/cli/ref_gemm.json   `mossq gemm --scheme mx2 --verify` report
+  tests/golden/cli/ref_gemm_pergroup.json  `mossq gemm --scheme pergroup --verify` report
 The GPU box never reads /root/reference; these files travel with the repo.
 """
 
@@ -38,13 +40,16 @@ def main():
     x = tensor_randn([64, 256], seed=5, dist="outlier_injected")
     tensor_write(x, os.path.join(d, "x.mosst"))
     r = CliRunner()
-    for scheme in ("mx2", "tensor"):
+    for scheme in ("mx2", "tensor", "group"):
         res = r.invoke(cli, ["quantize", "--scheme", scheme, "--in", os.path.join(d, "x.mosst"),
                              "--out", os.path.join(d, f"ref_{scheme}.mosst"),
                              "--meta", os.path.join(d, f"ref_{scheme}.json")])
         assert res.exit_code == 0, res.output
     res = r.invoke(cli, ["gemm", "--m", "128", "--n", "256", "--k", "512", "--scheme", "mx2", "--verify",
                          "--out", os.path.join(d, "ref_gemm.json")])
+    assert res.exit_code == 0, res.output
+    res = r.invoke(cli, ["gemm", "--m", "128", "--n", "256", "--k", "512", "--scheme", "pergroup", "--verify",
+                         "--out", os.path.join(d, "ref_gemm_pergroup.json")])
     assert res.exit_code == 0, res.output
     for f in os.listdir(d):
         if f.endswith(".manifest.json"):

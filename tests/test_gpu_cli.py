@@ -28,7 +28,7 @@ def _cli(*args):
     return r
 
 
-@pytest.mark.parametrize("scheme", ["mx2", "tensor"])
+@pytest.mark.parametrize("scheme", ["mx2", "tensor", "group"])
 def test_quantize_matches_reference_cli(tmp_path, scheme):
     out, meta = tmp_path / "q.mosst", tmp_path / "q.json"
     _cli("quantize", "--scheme", scheme, "--in", os.path.join(GOLD, "x.mosst"), "--out", str(out), "--meta", str(meta))
@@ -42,10 +42,12 @@ def test_quantize_matches_reference_cli(tmp_path, scheme):
     assert (tmp_path / "q.mosst.manifest.json").exists()
 
 
-def test_gemm_verify_matches_reference_report(tmp_path):
+@pytest.mark.parametrize("scheme", ["mx2", "pergroup"])
+def test_gemm_verify_matches_reference_report(tmp_path, scheme):
     out = tmp_path / "g.json"
-    r = _cli("gemm", "--m", "128", "--n", "256", "--k", "512", "--scheme", "mx2", "--verify", "--out", str(out))
-    got, ref = json.loads(out.read_text()), json.load(open(os.path.join(GOLD, "ref_gemm.json")))
+    r = _cli("gemm", "--m", "128", "--n", "256", "--k", "512", "--scheme", scheme, "--verify", "--out", str(out))
+    ref_name = "ref_gemm.json" if scheme == "mx2" else "ref_gemm_pergroup.json"
+    got, ref = json.loads(out.read_text()), json.load(open(os.path.join(GOLD, ref_name)))
     assert got["counters"] == ref["counters"]
     assert got["frobenius_rel_error"] <= 1e-5          # FP32 accumulation vs the float64 oracle
     assert "frobenius_rel_error=" in r.stdout
