@@ -37,6 +37,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "FP8 GEMM TFLOP/s, quantize GB/s; 7B-shape train tokens/s at 1/2/4/8 B200"
+LAYER_WORKLOAD = ("configs[1]: MOSS quantize + MXFP8 fwd/dgrad/wgrad GEMMs over the Llama-7B linear shapes "
+                  "(QKV 4096->12288, O 4096->4096, gate/up 4096->2x11008, down 11008->4096) + fused "
+                  "AdamW/autoscale/FP8-copy, as one training step")
 
 
 def parse():
@@ -117,7 +120,9 @@ def run_reference(args, rank: int) -> None:
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64 (reference numpy)", "data": "synthetic",
-            "config": {"workload": "MOSS FP8 linear training step (reference CPU dataflow sample)",
+            "config": {"workload": LAYER_WORKLOAD,
+                       "sample": f"bounded sample of that workload per step: one MOSS linear fwd+dgrad+wgrad+AdamW, "
+                                 f"tokens={tokens}, {d}x{d}, through the oracle port (reference numpy dataflow)",
                        "tokens": tokens, "shape": [d, d]},
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
                              "sample": f"per step: one MOSS linear fwd+dgrad+wgrad+AdamW, tokens={tokens}, "
@@ -496,9 +501,7 @@ def main() -> None:
         if e2e is not None:
             e2e = {**e2e, "value": world * T / (e2e["ms_per_step"] / 1e3), "unit": "tokens/s"}
     else:
-        wl = ("configs[1]: MOSS quantize + MXFP8 fwd/dgrad/wgrad GEMMs over the Llama-7B linear "
-              "shapes (QKV 4096->12288, O 4096->4096, gate/up 4096->2x11008, down 11008->4096) "
-              "+ fused AdamW/autoscale/FP8-copy, as one training step")
+        wl = LAYER_WORKLOAD
     line = {
         "metric": METRIC,
         "value": (world * T / (ms / 1e3)) if llama else world * flops_step / (ms / 1e3) / 1e12,
