@@ -83,6 +83,28 @@ __device__ __forceinline__ float div1(float x, float nb, float r) {
     return __fmaf_rn(r, __fmaf_rn(nb, q0, x), q0);
 }
 
+// Explicit shared-space accesses: the slot pointers come from a runtime-aligned
+// dynamic smem base, which the compiler can no longer prove is shared, so
+// plain C++ dereferences compile to generic 64-bit LD.E/ST.E (an IADD3.X pair
+// per access).  volatile: ordered after the mbarrier waits / barriers.
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.b8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 struct Q4Global {
     float g;         // global scale f32(amax/448), 0 -> 1
     uint32_t gbits;
@@ -263,10 +285,10 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
         for (int j = 0; j < n; ++j) {
             const int s = j % Q4_S;
             wait_slot(s);
-            const uint4* T = reinterpret_cast<const uint4*>(slots + s * Q4_IN);
+            const uint32_t T = smem_u32(slots + s * Q4_IN) + tid * 16;
 #pragma unroll
             for (int q = 0; q < Q4_IN / 16 / Q4_THREADS; ++q) {
-                const uint4 u = T[q * Q4_THREADS + tid];
+                const uint4 u = lds128(T + q * Q4_THREADS * 16);
                 m = __vmaxu2(m, u.x & 0x7FFF7FFFu);
                 m = __vmaxu2(m, u.y & 0x7FFF7FFFu);
                 m = __vmaxu2(m, u.z & 0x7FFF7FFFu);
@@ -359,15 +381,17 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
         const int j = desc ? n - 1 - p : p;
         const int s = j % Q4_S;
         if (!(desc && p < Q4_S)) wait_slot(s);     // resident tiles were waited in phase A
-        uint8_t* T = slots + s * Q4_IN;
-        uint8_t* sfs = sfst + (p & 1) * 1024;
+        uint8_t* Tg = slots + s * Q4_IN;               // generic: for the TMA store
+        const uint32_t T = smem_u32(Tg);
+        uint8_t* sfsg = sfst + (p & 1) * 1024;
+        const uint32_t sfs = smem_u32(sfsg);
         const int tile = b + j * G;
         const int r0 = (tile / ctiles) * Q4_T, c0 = (tile % ctiles) * Q4_T;
 
         uint32_t ucol[32];
         if (COL) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) ucol[i] = *reinterpret_cast<const uint32_t*>(T + cbase[i & 7] + i * 128);
+            for (int i = 0; i < 32; ++i) ucol[i] = lds32(T + cbase[i & 7] + i * 128);
         }
         uint32_t rcodes[2][8];
         if (ROW) {
@@ -376,11 +400,11 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
                 uint32_t w[16];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const uint4 u = *reinterpret_cast<const uint4*>(T + h * 16384 + (rbase ^ (uint32_t)(q << 4)));
+                    const uint4 u = lds128(T + h * 16384 + (rbase ^ (uint32_t)(q << 4)));
                     w[4 * q] = u.x; w[4 * q + 1] = u.y; w[4 * q + 2] = u.z; w[4 * q + 3] = u.w;
                 }
                 const uint32_t code = q4_block(w, Gs, rerr, rcodes[h]);
-                sfs[sfo_row + 2 * h] = (uint8_t)code;
+                sts8(sfs + sfo_row + 2 * h, code);
                 if (MICRO && micro) micro[(int64_t)(r0 + rr) * (cols >> 5) + (c0 >> 5) + kb0 + 2 * h] = (uint8_t)code;
             }
         }
@@ -388,14 +412,13 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
         if (ROW) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                *reinterpret_cast<uint4*>(T + (obase ^ (uint32_t)((4 * h) << 4))) =
-                    make_uint4(rcodes[h][0], rcodes[h][1], rcodes[h][2], rcodes[h][3]);
-                *reinterpret_cast<uint4*>(T + (obase ^ (uint32_t)((4 * h + 1) << 4))) =
-                    make_uint4(rcodes[h][4], rcodes[h][5], rcodes[h][6], rcodes[h][7]);
+                sts128(T + (obase ^ (uint32_t)((4 * h) << 4)), rcodes[h][0], rcodes[h][1], rcodes[h][2], rcodes[h][3]);
+                sts128(T + (obase ^ (uint32_t)((4 * h + 1) << 4)), rcodes[h][4], rcodes[h][5], rcodes[h][6],
+                       rcodes[h][7]);
             }
         }
         if (COL) {
-            uint8_t* Tc = T + 16384;
+            const uint32_t Tc = T + 16384;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 // column 2cp+h: rows i, i+1 packed as one pair word
@@ -406,9 +429,9 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
                              : __byte_perm(ucol[2 * i], ucol[2 * i + 1], 0x5410);
                 uint32_t cc[8];
                 const uint32_t code = q4_block(w, Gs, rerr, cc);
-                *reinterpret_cast<uint4*>(Tc + cob[h]) = make_uint4(cc[0], cc[1], cc[2], cc[3]);
-                *reinterpret_cast<uint4*>(Tc + (cob[h] ^ 16u)) = make_uint4(cc[4], cc[5], cc[6], cc[7]);
-                sfs[sfo_col[h]] = (uint8_t)code;
+                sts128(Tc + cob[h], cc[0], cc[1], cc[2], cc[3]);
+                sts128(Tc + (cob[h] ^ 16u), cc[4], cc[5], cc[6], cc[7]);
+                sts8(sfs + sfo_col[h], code);
                 if (MICRO && micro_t)
                     micro_t[(int64_t)(c0 + 2 * cp + h) * (rows >> 5) + (r0 >> 5) + rb] = (uint8_t)code;
             }
@@ -417,12 +440,12 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
         __syncthreads();
         if (tid == 0) {
             if (ROW) {
-                tma_store_2d(&tm_codes, T, c0, r0);
-                if (sf) bulk_store(sf + ((int64_t)(r0 >> 7) * kch_row + (c0 >> 7)) * 512, sfs, 512);
+                tma_store_2d(&tm_codes, Tg, c0, r0);
+                if (sf) bulk_store(sf + ((int64_t)(r0 >> 7) * kch_row + (c0 >> 7)) * 512, sfsg, 512);
             }
             if (COL) {
-                tma_store_2d(&tm_codes_t, T + 16384, r0, c0);
-                if (sf_t) bulk_store(sf_t + ((int64_t)(c0 >> 7) * kch_t + (r0 >> 7)) * 512, sfs + 512, 512);
+                tma_store_2d(&tm_codes_t, Tg + 16384, r0, c0);
+                if (sf_t) bulk_store(sf_t + ((int64_t)(c0 >> 7) * kch_t + (r0 >> 7)) * 512, sfsg + 512, 512);
             }
             bulk_commit();
             // the store of position p-1 has read its slot and SF staging -> refill the slot with p+2
