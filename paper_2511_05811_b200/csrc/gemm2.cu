@@ -267,6 +267,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
         const int cq = ew >> 2;               // column slice of the 256-column tile
         const uint32_t tmem_empty_leader = mapa_shared(tmem_empty, 0);
         uint8_t* stg = s_stg + ew * L::STG_BYTES;
+        const uint32_t stg_s = smem_u32(stg);
         const float alpha = __fmul_rn(*sA, *sB);
         uint32_t acc_phase = 0;
         int it_ = 0;
@@ -347,7 +348,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                             o.z = __float_as_uint(__uint_as_float(q[2]) * alpha);
                             o.w = __float_as_uint(__uint_as_float(q[3]) * alpha);
                         }
-                        *reinterpret_cast<uint4*>(stg + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) = o;
+                        sts128(stg_s + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4), o.x, o.y, o.z, o.w);
                     }
                     fence_proxy_async_smem();
                     __syncwarp();

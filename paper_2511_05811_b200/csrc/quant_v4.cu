@@ -83,28 +83,6 @@ __device__ __forceinline__ float div1(float x, float nb, float r) {
     return __fmaf_rn(r, __fmaf_rn(nb, q0, x), q0);
 }
 
-// Explicit shared-space accesses: the slot pointers come from a runtime-aligned
-// dynamic smem base, which the compiler can no longer prove is shared, so
-// plain C++ dereferences compile to generic 64-bit LD.E/ST.E (an IADD3.X pair
-// per access).  volatile: ordered after the mbarrier waits / barriers.
-__device__ __forceinline__ uint32_t lds32(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ uint4 lds128(uint32_t a) {
-    uint4 v;
-    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a)
-                 : "memory");
-    return v;
-}
-__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
-}
-__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
-    asm volatile("st.shared.b8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-
 struct Q4Global {
     float g;         // global scale f32(amax/448), 0 -> 1
     uint32_t gbits;
