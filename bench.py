@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--seq", type=int, default=4096, help="llama7b: sequence length (batch 1 per GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-llama", action="store_true",
+                    help="layer workload: skip the Llama-2-7B-shape tokens/s sub-measurement (configs[3])")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
     ap.add_argument("--zero1", action="store_true",
                     help="N>1: ZeRO-1 (reduce-scatter grads, sharded K3, FP8 all-gather) instead of all-reduce DP")
@@ -225,6 +227,23 @@ def quantizer_rates(dev, tokens: int, hbm: float) -> dict:
     res["how"] = ("the 8 row+col quantizations of one layer step at M=%d, 10 back-to-back launches each (inputs > "
                   "L2 are re-read by the single-launch mode), algorithmic bytes 4.063 B/elem" % tokens)
     return res
+
+
+def llama7b_submeasure() -> dict:
+    """The metric's third component (7B-shape train tokens/s, configs[3]):
+    the full Llama-2-7B-shape decoder step (32 layers, seq 4096, batch 1,
+    MOSS FP8 linears, CUDA-graph replays), measured in a child process so its
+    ~160 GB do not share the allocator with the layer workload."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--workload", "llama7b", "--steps", "6", "--warmup", "3",
+           "--no-cpu-baseline", "--no-e2e"]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+        return {"tokens_per_s": d["value"], "ms_per_step": d["ms_per_step"], "steps": d["steps"],
+                "config": d["config"]["workload"], "gemm_tflops_in_step": d["roofline"]["achieved"],
+                "gemm_share_of_step": d["roofline"]["share_of_step"], "clocks": d["clocks"]}
+    except Exception as ex:  # noqa: BLE001 - a sub-measurement must not sink the bench line
+        return {"error": str(ex)[:200]}
 
 
 # ------------------------------------------------------------------ clocks
@@ -554,6 +573,8 @@ def main() -> None:
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_sample(1024, 4096)
         line["cpu_baseline"].pop("seconds", None)
+    if not llama and not args.no_llama and world == 1:
+        line["llama7b"] = llama7b_submeasure()
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
