@@ -178,6 +178,13 @@ int moss_swiglu_bwd(const void* dh, const void* gu, void* dgu, float* amax, int6
  * rotated by cos/sin [S_max, hd/2] (f32) at position s */
 int moss_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q, void* k, void* v, int64_t B,
                   int64_t S, int64_t H, int64_t hd, void* stream);
+/* Cross entropy of bf16 logits [T, V] (V % 8 == 0) against int64 targets:
+ * fwd  lse[t] = logsumexp(x[t, :]) (f32, one read of the row), loss[t] = lse[t] - x[t, y_t]
+ * bwd  dlogits = (softmax(x) - onehot(y)) * (*scale), bf16; scale a device f32 (dL/dmean / T) */
+int moss_cross_entropy_fwd(const void* logits, const int64_t* targets, float* lse, float* loss, int64_t T, int64_t V,
+                           void* stream);
+int moss_cross_entropy_bwd(const void* logits, const int64_t* targets, const float* lse, const float* scale,
+                           void* dlogits, int64_t T, int64_t V, void* stream);
 /* dq, dk, dv [B, H, S, hd] -> dqkv [B, S, 3, H, hd] (inverse rotation) */
 int moss_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
                   float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, void* stream);

@@ -45,6 +45,8 @@ _SIGS = {
     "moss_rope_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
     "moss_rope_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
     "moss_transpose_u8": (_I, [_P, _P, _I64, _I64, _P]),
+    "moss_cross_entropy_fwd": (_I, [_P, _P, _P, _P, _I64, _I64, _P]),
+    "moss_cross_entropy_bwd": (_I, [_P, _P, _P, _P, _P, _I64, _I64, _P]),
     "moss_quant_per_group": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P, _P]),
     "moss_gemm_pergroup": (_I, [_P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _P]),
     "moss_encode_scaled": (_I, [_P, _I, _I64, _I64, _P, _F, _I, _P, _P, _P, _P, _P, _P]),
@@ -362,3 +364,17 @@ def gemm_pergroup(a, sa_t, b, sb_t, d) -> None:
     with _Span("gemm_pg", 2.0 * m * n * k):
         check(lib().moss_gemm_pergroup(a.data_ptr(), sa_t.data_ptr(), b.data_ptr(), sb_t.data_ptr(), d.data_ptr(),
                                        dtype_code(d), d.stride(0), m, n, k, stream()), "moss_gemm_pergroup")
+
+
+def cross_entropy_fwd(logits, targets, lse, loss) -> None:
+    T, V = logits.shape
+    with _Span("producer", T * V * 2):
+        check(lib().moss_cross_entropy_fwd(logits.data_ptr(), targets.data_ptr(), lse.data_ptr(), loss.data_ptr(),
+                                           T, V, stream()), "moss_cross_entropy_fwd")
+
+
+def cross_entropy_bwd(logits, targets, lse, scale, dlogits) -> None:
+    T, V = logits.shape
+    with _Span("producer", T * V * 4):
+        check(lib().moss_cross_entropy_bwd(logits.data_ptr(), targets.data_ptr(), lse.data_ptr(), scale.data_ptr(),
+                                           dlogits.data_ptr(), T, V, stream()), "moss_cross_entropy_bwd")

@@ -35,6 +35,10 @@ int launch_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void*
 int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
                     float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, cudaStream_t st);
 int launch_transpose_u8(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t st);
+int launch_xent_fwd(const void* logits, const int64_t* targets, float* lse, float* loss, int64_t T, int64_t V,
+                    cudaStream_t st);
+int launch_xent_bwd(const void* logits, const int64_t* targets, const float* lse, const float* scale, void* dlogits,
+                    int64_t T, int64_t V, cudaStream_t st);
 int launch_quant_per_group(const void* x, int dtype, int64_t rows, int64_t cols, uint8_t* codes, float* scales,
                            uint32_t* flags, cudaStream_t st);
 int launch_gemm_pergroup(const uint8_t* A, const float* sa_t, const uint8_t* B, const float* sb_t, void* D,
@@ -220,6 +224,22 @@ int moss_transpose_u8(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t co
     if (!src || !dst) return MOSS_ERR_ARGUMENT;
     if (!aligned(src, 16) || !aligned(dst, 16) || cols % 16 || rows % 16) return MOSS_ERR_ALIGN;
     return moss::launch_transpose_u8(src, dst, rows, cols, (cudaStream_t)stream);
+}
+
+int moss_cross_entropy_fwd(const void* logits, const int64_t* targets, float* lse, float* loss, int64_t T, int64_t V,
+                           void* stream) {
+    if (T <= 0 || V <= 0 || V % 8 || T > INT32_MAX || V > INT32_MAX) return MOSS_ERR_SHAPE;
+    if (!logits || !targets || !lse || !loss) return MOSS_ERR_ARGUMENT;
+    if (!al16(logits)) return MOSS_ERR_ALIGN;
+    return moss::launch_xent_fwd(logits, targets, lse, loss, T, V, (cudaStream_t)stream);
+}
+
+int moss_cross_entropy_bwd(const void* logits, const int64_t* targets, const float* lse, const float* scale,
+                           void* dlogits, int64_t T, int64_t V, void* stream) {
+    if (T <= 0 || V <= 0 || V % 8 || T > INT32_MAX || V > INT32_MAX) return MOSS_ERR_SHAPE;
+    if (!logits || !targets || !lse || !scale || !dlogits) return MOSS_ERR_ARGUMENT;
+    if (!al16(logits) || !al16(dlogits)) return MOSS_ERR_ALIGN;
+    return moss::launch_xent_bwd(logits, targets, lse, scale, dlogits, T, V, (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------- per-group comparator (COAT-style)

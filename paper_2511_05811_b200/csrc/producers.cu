@@ -443,6 +443,77 @@ __global__ void __launch_bounds__(256) rope_bwd_kernel(const __nv_bfloat16* __re
     block_amax_commit(m, red_u, amax);
 }
 
+// ------------------------------------------------------------------ cross entropy (LM head)
+// forward: one CTA per row of bf16 logits [T, V]: online max / sum-exp in f32
+// (one read of the row), lse[t] = max + log(sum), loss[t] = lse[t] - x[t, y_t]
+__global__ void __launch_bounds__(256) xent_fwd_kernel(const __nv_bfloat16* __restrict__ logits,
+                                                       const int64_t* __restrict__ targets, float* __restrict__ lse,
+                                                       float* __restrict__ loss, int V) {
+    __shared__ float red_m[8], red_s[8];
+    const int64_t t = blockIdx.x;
+    const __nv_bfloat16* row = logits + t * V;
+    float m = -INFINITY, sum = 0.f;
+    const int nv = V / 8;
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+        float v[8];
+        bf16x8_load(row + i * 8, v);
+        float vm = v[0];
+#pragma unroll
+        for (int j = 1; j < 8; ++j) vm = fmaxf(vm, v[j]);
+        const float nm = fmaxf(m, vm);
+        sum *= __expf(m - nm);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sum += __expf(v[j] - nm);
+        m = nm;
+    }
+    // merge (m, sum) pairs: warp, then CTA
+    // (threads without elements carry (-inf, 0): their terms are skipped, exp(-inf - -inf) would be NaN)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float om = __shfl_xor_sync(0xFFFFFFFFu, m, o), os = __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+        const float nm = fmaxf(m, om);
+        sum = (m == -INFINITY ? 0.f : sum * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+        m = nm;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        red_m[warp] = m;
+        red_s[warp] = sum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float M = red_m[0], S = red_s[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            if (red_m[w] == -INFINITY) continue;
+            const float nm = fmaxf(M, red_m[w]);
+            S = (M == -INFINITY ? 0.f : S * __expf(M - nm)) + red_s[w] * __expf(red_m[w] - nm);
+            M = nm;
+        }
+        const float l = M + __logf(S);
+        lse[t] = l;
+        loss[t] = l - __bfloat162float(row[targets[t]]);
+    }
+}
+
+// backward: dlogits[t, v] = (exp(x - lse[t]) - [v == y_t]) * (*scale)   (scale = dL/dloss / T)
+__global__ void __launch_bounds__(256) xent_bwd_kernel(const __nv_bfloat16* __restrict__ logits,
+                                                       const int64_t* __restrict__ targets,
+                                                       const float* __restrict__ lse, const float* __restrict__ scale,
+                                                       __nv_bfloat16* __restrict__ dlogits, int V) {
+    const int64_t t = blockIdx.x;
+    const float l = lse[t], sc = *scale;
+    const int64_t y = targets[t];
+    const __nv_bfloat16* row = logits + t * V;
+    __nv_bfloat16* out = dlogits + t * V;
+    for (int i = threadIdx.x; i < V / 8; i += blockDim.x) {
+        float v[8];
+        bf16x8_load(row + i * 8, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = (__expf(v[j] - l) - ((int64_t)(i * 8 + j) == y ? 1.f : 0.f)) * sc;
+        *reinterpret_cast<uint4*>(out + i * 8) = bf16x8_pack(v);
+    }
+}
+
 // ------------------------------------------------------------------ launchers
 template <typename K>
 static int resident(K kern, int threads) {
@@ -565,6 +636,19 @@ int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float*
     rope_bwd_kernel<<<dim3((unsigned)(B * S), (unsigned)((H * (hd / 8) + 255) / 256)), 256, 0, st>>>(
         (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv, cosv, sinv,
         (__nv_bfloat16*)dqkv, reinterpret_cast<uint32_t*>(amax), (int)B, (int)S, (int)H, (int)hd);
+    return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+}
+
+int launch_xent_fwd(const void* logits, const int64_t* targets, float* lse, float* loss, int64_t T, int64_t V,
+                    cudaStream_t st) {
+    xent_fwd_kernel<<<(unsigned)T, 256, 0, st>>>((const __nv_bfloat16*)logits, targets, lse, loss, (int)V);
+    return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+}
+
+int launch_xent_bwd(const void* logits, const int64_t* targets, const float* lse, const float* scale, void* dlogits,
+                    int64_t T, int64_t V, cudaStream_t st) {
+    xent_bwd_kernel<<<(unsigned)T, 256, 0, st>>>((const __nv_bfloat16*)logits, targets, lse, scale,
+                                                 (__nv_bfloat16*)dlogits, (int)V);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 

@@ -23,7 +23,7 @@ import torch.nn.functional as F
 from torch import nn
 
 from .nn import MossLinear
-from .producers import AddRMSNormFn, RMSNormFn, RopeQKVFn, SwiGLUFn
+from .producers import AddRMSNormFn, CrossEntropyFn, RMSNormFn, RopeQKVFn, SwiGLUFn
 
 __all__ = ["LlamaConfig", "LlamaModel", "MarkovTokens", "LLAMA_125M", "LLAMA2_7B"]
 
@@ -187,6 +187,8 @@ class LlamaModel(nn.Module):
         logits = F.linear(x, self.head.to(self.cfg.compute_dtype))
         if targets is None:
             return logits
+        if self.blocks[0].fused and logits.dtype == torch.bfloat16 and logits.shape[-1] % 8 == 0:
+            return CrossEntropyFn.apply(logits, targets)       # fused f32 log-softmax on the bf16 logits
         lg = logits if logits.dtype == torch.float64 else logits.float()
         return F.cross_entropy(lg.reshape(-1, lg.shape[-1]), targets.reshape(-1))
 

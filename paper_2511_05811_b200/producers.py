@@ -19,7 +19,7 @@ import torch
 
 from . import _lib
 
-__all__ = ["RMSNormFn", "AddRMSNormFn", "SwiGLUFn", "RopeQKVFn"]
+__all__ = ["RMSNormFn", "AddRMSNormFn", "SwiGLUFn", "RopeQKVFn", "CrossEntropyFn"]
 
 
 def _c2(t: torch.Tensor, d: int) -> torch.Tensor:
@@ -142,3 +142,30 @@ class RopeQKVFn(torch.autograd.Function):
         dqkv = torch.empty(B, S, 3 * H * hd, dtype=dq.dtype, device=dq.device)
         _lib.rope_bwd(dq, dk, dv, cos, sin, dqkv, _amax_buf(ctx.consumer, dqkv.view(B * S, -1)), B, S, H, hd)
         return dqkv, None, None, None, None
+
+
+class CrossEntropyFn(torch.autograd.Function):
+    """mean_t (logsumexp(x_t) - x_t[y_t]) on bf16 logits [T, V] in f32 math,
+    one read of the logits forward, one read + one bf16 write backward (the
+    torch path materialises an f32 copy of the logits and an f32 gradient)."""
+
+    @staticmethod
+    def forward(ctx, logits, targets):
+        V = logits.shape[-1]
+        lg = _c2(logits, V)
+        tg = targets.reshape(-1).contiguous()
+        T = lg.shape[0]
+        lse = torch.empty(T, dtype=torch.float32, device=lg.device)
+        loss = torch.empty(T, dtype=torch.float32, device=lg.device)
+        _lib.cross_entropy_fwd(lg, tg, lse, loss)
+        ctx.save_for_backward(lg, tg, lse)
+        ctx.shape = logits.shape
+        return loss.mean()
+
+    @staticmethod
+    def backward(ctx, g):
+        lg, tg, lse = ctx.saved_tensors
+        scale = (g.float() / lg.shape[0]).reshape(1).contiguous()
+        d = torch.empty_like(lg)
+        _lib.cross_entropy_bwd(lg, tg, lse, scale, d)
+        return d.view(ctx.shape), None

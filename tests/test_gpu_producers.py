@@ -162,3 +162,18 @@ def test_fused_block_matches_torch_glue_and_uses_producer_amax(monkeypatch):
         cos = float(torch.dot(a, b) / (a.norm() * b.norm() + 1e-12))
         assert rel < 0.15 and cos > 0.99, (n, rel, cos)
     mnn.raise_if_flagged("cuda", "fused block")
+
+
+@pytest.mark.parametrize("T,V", [(64, 512), (64, 1000), (1024, 32000), (4096, 32000)])
+def test_cross_entropy_fused(T, V):
+    from paper_2511_05811_b200.producers import CrossEntropyFn
+    torch.manual_seed(T)
+    logits = (torch.randn(T, V, device="cuda") * 3).to(torch.bfloat16).requires_grad_(True)
+    tg = torch.randint(0, V, (T,), device="cuda")
+    loss = CrossEntropyFn.apply(logits, tg)
+    lf = logits.detach().float().requires_grad_(True)
+    ref = F.cross_entropy(lf, tg)
+    assert abs(float(loss) - float(ref)) <= 1e-5 * abs(float(ref)) + 1e-6
+    (loss * 2.0).backward()
+    (ref * 2.0).backward()
+    close_bf16(logits.grad, lf.grad, rtol=2 ** -7, atol=1e-8)
