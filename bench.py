@@ -64,13 +64,23 @@ def parse():
 
 
 # ------------------------------------------------------------------ CPU oracle leg
-def cpu_linear_step(tokens: int, d_in: int, d_out: int, seed: int = 0) -> float:
+def cpu_linear_step(tokens: int, d_in: int, d_out: int, seed: int = 0, ops: dict | None = None) -> float:
     """One MOSS linear fwd + dgrad + wgrad + AdamW/autoscale step through the
     CPU oracle (the reference's numpy dataflow: per-32-block float64 GEMMs,
-    gemm.py:115-129; float64 AdamW, optim.py:78-106).  Returns seconds."""
+    gemm.py:115-129; float64 AdamW, optim.py:78-106).  Returns seconds; the
+    per-op seconds (quant_two_level, weight encode,
+    gemm_mx_epilogue, adamw_step, auto_scale_advance) accumulate into ``ops``."""
     import numpy as np
 
     from oracle import numpy_ref as R
+
+    ops = {} if ops is None else ops
+
+    def timed(name, fn, *a):
+        t = time.perf_counter()
+        r = fn(*a)
+        ops[name] = ops.get(name, 0.0) + time.perf_counter() - t
+        return r
 
     rng = np.random.default_rng(seed)
     x = rng.standard_normal((tokens, d_in)).astype(np.float32)
@@ -79,32 +89,37 @@ def cpu_linear_step(tokens: int, d_in: int, d_out: int, seed: int = 0) -> float:
     st = R.adam_init(w.shape, eta=3e-4, weight_decay=0.1)
     sched = R.Schedule(s_t=R.jit_scale(w))
     t0 = time.perf_counter()
-    wc, _ = R.encode_weight(w, sched.s_t)                       # train.py:168
-    qx = R.quant_two_level(x)                                   # train.py:171
-    R.gemm_mx_epilogue(wc, sched.s_t, qx)                        # fwd
-    qdy = R.quant_two_level(dy)
-    R.gemm_mx_epilogue(np.ascontiguousarray(wc.T), sched.s_t, qdy)   # dgrad
-    qdy_t = R.quant_two_level(np.ascontiguousarray(dy.T))
-    qx_t = R.quant_two_level(np.ascontiguousarray(x.T))
-    a = R.dequantize_two_level(qdy_t)
-    b = R.fp8_decode(qx_t.codes).astype(np.float64)
-    ss = R.e8m0_decode(qx_t.micro_codes).astype(np.float64)
-    dw = np.zeros((d_out, d_in))
-    for blk in range(tokens // 32):                             # wgrad, same block dataflow
-        sl = slice(blk * 32, (blk + 1) * 32)
-        dw += (a[:, sl] @ b[:, sl].T) * ss[None, :, blk]
-    dw *= qx_t.global_scale
-    w, _ = R.adamw_step(w, dw, st)                              # optim.py:78-106
-    R.advance(sched, 3e-4)                                      # autoscale.py:71-79
+    wc, _ = timed("weight_encode", R.encode_weight, w, sched.s_t)                  # train.py:168
+    qx = timed("quant_two_level", R.quant_two_level, x)                             # train.py:171
+    timed("gemm_mx_epilogue", R.gemm_mx_epilogue, wc, sched.s_t, qx)                # fwd
+    qdy = timed("quant_two_level", R.quant_two_level, dy)
+    timed("gemm_mx_epilogue", R.gemm_mx_epilogue, np.ascontiguousarray(wc.T), sched.s_t, qdy)   # dgrad
+    qdy_t = timed("quant_two_level", R.quant_two_level, np.ascontiguousarray(dy.T))
+    qx_t = timed("quant_two_level", R.quant_two_level, np.ascontiguousarray(x.T))
+
+    def wgrad():
+        a = R.dequantize_two_level(qdy_t)
+        b = R.fp8_decode(qx_t.codes).astype(np.float64)
+        ss = R.e8m0_decode(qx_t.micro_codes).astype(np.float64)
+        dw = np.zeros((d_out, d_in))
+        for blk in range(tokens // 32):                         # wgrad, same block dataflow
+            sl = slice(blk * 32, (blk + 1) * 32)
+            dw += (a[:, sl] @ b[:, sl].T) * ss[None, :, blk]
+        return dw * qx_t.global_scale
+    dw = timed("gemm_mx_epilogue", wgrad)
+    w, _ = timed("adamw_step", R.adamw_step, w, dw, st)                             # optim.py:78-106
+    timed("auto_scale_advance", R.advance, sched, 3e-4)                             # autoscale.py:71-79
     return time.perf_counter() - t0
 
 
 def cpu_sample(tokens: int, d: int, reps: int = 1) -> dict:
-    secs = min(cpu_linear_step(tokens, d, d, seed=r) for r in range(reps))
+    ops: dict = {}
+    secs = min(cpu_linear_step(tokens, d, d, seed=r, ops=ops) for r in range(reps))
     flops = 6.0 * tokens * d * d
     return {"value": flops / secs / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
             "sample": f"one MOSS linear fwd+dgrad+wgrad+AdamW step, tokens={tokens}, {d}x{d}, oracle/numpy_ref "
                       f"(reference numpy dataflow, float64 block GEMMs), {secs:.2f} s",
+            "per_op_seconds": {k: round(v / reps, 4) for k, v in ops.items()},
             "seconds": secs}
 
 
