@@ -53,15 +53,18 @@ __device__ __forceinline__ unsigned long long g2_now() {
 #endif
 
 constexpr int G2_BM = 128;       // rows per CTA (256 per pair)
-constexpr int G2_BN = 256;       // columns per pair tile
+constexpr int G2_BN = 256;       // columns per pair tile (the default; 128 with 2 accumulator stages)
 constexpr int G2_BK = 128;
 
-template <int STAGES, bool TMA_EPI, int EPI_WARPS>
+// BN = 256: one TMEM accumulator (256 columns + SF); BN = 128: two accumulator
+// stages (2 x 128 columns) so the epilogue of tile i overlaps tile i+1's MMAs.
+template <int STAGES, bool TMA_EPI, int EPI_WARPS, int BN>
 struct G2Layout {
+    static constexpr int ACC = BN == 128 ? 2 : 1;              // TMEM accumulator stages
     static constexpr int A_BYTES = G2_BM * G2_BK;              // 16 KB
-    static constexpr int B_BYTES = (G2_BN / 2) * G2_BK;        // 16 KB (half of B per CTA)
+    static constexpr int B_BYTES = (BN / 2) * G2_BK;           // half of B per CTA
     static constexpr int SFA_BYTES = 512;
-    static constexpr int SFB_BYTES = (G2_BN / 128) * 512;      // scales of all 256 B rows in each CTA
+    static constexpr int SFB_BYTES = (BN / 128) * 512;         // scales of all BN B rows in each CTA
     static constexpr int OFF_A = 0;
     static constexpr int OFF_B = OFF_A + STAGES * A_BYTES;
     static constexpr int OFF_SFA = OFF_B + STAGES * B_BYTES;
@@ -70,10 +73,10 @@ struct G2Layout {
     static constexpr int STG_BYTES = TMA_EPI ? 2048 : 0;       // per epilogue warp: 32 rows x 64 B
     static constexpr int OFF_STG = OFF_UNIT + SFB_BYTES;
     static constexpr int OFF_BAR = OFF_STG + EPI_WARPS * STG_BYTES;
-    static constexpr int N_BARS = 2 * STAGES + 2;             // full, empty, tmem_full, tmem_empty
+    static constexpr int N_BARS = 2 * STAGES + 2 * ACC;       // full, empty, tmem_full[ACC], tmem_empty[ACC]
     static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
     static constexpr int SMEM = OFF_TMEM + 16 + 1024;
-    static constexpr uint32_t TMEM_COLS = 512;                 // 256 accumulator + SF columns
+    static constexpr uint32_t TMEM_COLS = 512;                 // ACC * BN = 256 accumulator + SF columns
 };
 
 // Tile raster: groups of G2_GROUP_M m-pairs walked n-major, so the ~74
@@ -94,15 +97,16 @@ __device__ __forceinline__ void g2_tile_coords(int tile, int m_pairs, int n_tile
 // SF buffers are viewed as [bytes/256, 256] u8 tensors: one 512 B chunk = box {256, 2}
 __device__ __forceinline__ int sf_row_of_chunk(int64_t chunk) { return (int)(chunk * 2); }
 
-template <bool OUT_BF16, int STAGES, bool TMA_EPI, int EPI_WARPS>
+template <bool OUT_BF16, int STAGES, bool TMA_EPI, int EPI_WARPS, int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32, 1)
     gemm_mxf8_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
                           const __grid_constant__ CUtensorMap tmD, void* __restrict__ D, int64_t ldd,
                           const float* __restrict__ sA, const float* __restrict__ sB, int M, int N, int K,
                           int unit_b, int accumulate) {
-    using L = G2Layout<STAGES, TMA_EPI, EPI_WARPS>;
-    constexpr int COLS = G2_BN / (EPI_WARPS / 4);   // accumulator columns per epilogue warp
+    using L = G2Layout<STAGES, TMA_EPI, EPI_WARPS, BN>;
+    constexpr int ACC = L::ACC;
+    constexpr int COLS = BN / (EPI_WARPS / 4);      // accumulator columns per epilogue warp
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* s_a = smem + L::OFF_A;
@@ -113,15 +117,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
     uint8_t* s_stg = smem + L::OFF_STG;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);   // the leader's are live
     uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;
-    uint64_t* tmem_empty = tmem_full + 1;                              // the leader's is live
+    uint64_t* tmem_full = empty + STAGES;                              // [ACC]
+    uint64_t* tmem_empty = tmem_full + ACC;                            // [ACC], the leader's are live
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
     const bool leader = rank == 0;
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-    const int m_pairs = M / (2 * G2_BM), n_tiles = N / G2_BN, num_tiles = m_pairs * n_tiles;
+    const int m_pairs = M / (2 * G2_BM), n_tiles = N / BN, num_tiles = m_pairs * n_tiles;
     const int kblocks = K / G2_BK;
 
     if (warp == 0 && lane == 0) {
@@ -136,8 +140,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
             mbar_init(&full[s], 1);        // leader's arrive.expect_tx; bytes from both CTAs
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
-        mbar_init(tmem_empty, 2 * EPI_WARPS);
+        for (int a = 0; a < ACC; ++a) {
+            mbar_init(&tmem_full[a], 1);
+            mbar_init(&tmem_empty[a], 2 * EPI_WARPS);
+        }
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc_2cta(tmem_slot, L::TMEM_COLS);
@@ -150,8 +156,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     // SF columns double-buffered by k-block parity: [256, 268) and [272, 284)
-    const uint32_t tm_sfa = tmem + G2_BN;
-    const uint32_t tm_sfb = tmem + G2_BN + 4;
+    const uint32_t tm_sfa = tmem + ACC * BN;
+    const uint32_t tm_sfb = tmem + ACC * BN + 4;
     constexpr uint32_t SF_ALT = 16;
 
     if (warp == 0) {
@@ -164,7 +170,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
             int mp, nt;
             g2_tile_coords(tile, m_pairs, n_tiles, mp, nt);
             const int mb = mp * 2 + rank;                       // this CTA's 128-row block of A
-            const int n0 = nt * G2_BN + rank * (G2_BN / 2);     // this CTA's half of B
+            const int n0 = nt * BN + rank * (BN / 2);           // this CTA's half of B
             for (int kb = 0; kb < kblocks; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 if (elect_one()) {
@@ -176,9 +182,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                                     sf_row_of_chunk((int64_t)mb * kblocks + kb));
                     if (!unit_b) {
 #pragma unroll
-                        for (int j = 0; j < G2_BN / 128; ++j)
+                        for (int j = 0; j < BN / 128; ++j)
                             tma_load_2d_2sm(s_sfb + stage * L::SFB_BYTES + j * 512, &tmSFB, fl, 0,
-                                            sf_row_of_chunk((int64_t)(nt * (G2_BN / 128) + j) * kblocks + kb));
+                                            sf_row_of_chunk((int64_t)(nt * (BN / 128) + j) * kblocks + kb));
                     }
                 }
                 __syncwarp();
@@ -194,7 +200,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
             if (unit_b) {
                 if (elect_one()) {
 #pragma unroll
-                    for (int j = 0; j < G2_BN / 128; ++j) {
+                    for (int j = 0; j < BN / 128; ++j) {
                         tmem_cp_sf_2cta(tm_sfb + j * 4, umma_desc(smem_u32(s_unit + j * 512), 0, 128, kLayoutNone));
                         tmem_cp_sf_2cta(tm_sfb + SF_ALT + j * 4,
                                         umma_desc(smem_u32(s_unit + j * 512), 0, 128, kLayoutNone));
@@ -203,8 +209,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                 __syncwarp();
             }
             int stage = 0;
-            uint32_t phase = 0, acc_phase = 0, sfbuf = 0;
-            constexpr uint32_t idesc0 = mxf8_idesc(2 * G2_BM, G2_BN, 0, 0);
+            uint32_t phase = 0, acc_phase = 0, sfbuf = 0;   // acc_phase bit a: parity of accumulator stage a
+            constexpr uint32_t idesc0 = mxf8_idesc(2 * G2_BM, BN, 0, 0);
             const uint64_t adesc0 = umma_desc(smem_u32(s_a), 0, 1024, kLayoutSW128);
             const uint64_t bdesc0 = umma_desc(smem_u32(s_b), 0, 1024, kLayoutSW128);
             const uint64_t sfadesc0 = umma_desc(smem_u32(s_sfa), 0, 128, kLayoutNone);
@@ -213,7 +219,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                 tmem_cp_sf_2cta(sa, sfadesc0 + (uint64_t)((stage * L::SFA_BYTES) >> 4));
                 if (!unit_b) {
 #pragma unroll
-                    for (int j = 0; j < G2_BN / 128; ++j)
+                    for (int j = 0; j < BN / 128; ++j)
                         tmem_cp_sf_2cta(sb + j * 4, sfbdesc0 + (uint64_t)((stage * L::SFB_BYTES + j * 512) >> 4));
                 }
             };
@@ -227,7 +233,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                 tc_fence_after();
                 if (elect_one()) copy_sf(tm_sfa + sfbuf, tm_sfb + sfbuf);
                 __syncwarp();
-                mbar_wait(tmem_empty, acc_phase ^ 1);
+                const int acc = ACC == 1 ? 0 : (it_ & 1);
+                mbar_wait(&tmem_empty[acc], ((acc_phase >> acc) & 1u) ^ 1u);
                 tc_fence_after();
                 if (lane == 0) G2_STAMP(pair, it_, 0);
                 for (int kb = 0; kb < kblocks; ++kb) {
@@ -242,7 +249,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                         const uint64_t bdesc = bdesc0 + (uint64_t)((stage * L::B_BYTES) >> 4);
 #pragma unroll
                         for (int k = 0; k < G2_BK / 32; ++k)
-                            mma_mxf8_2cta(tmem, adesc + 2 * k, bdesc + 2 * k,
+                            mma_mxf8_2cta(tmem + acc * BN, adesc + 2 * k, bdesc + 2 * k,
                                           idesc0 | ((uint32_t)k << 29) | ((uint32_t)k << 4), sa, sb, (kb | k) != 0);
                         tc_commit_2cta_mc(&empty[stage], 0x3);
                     }
@@ -254,10 +261,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                         phase ^= 1;
                     }
                 }
-                if (elect_one()) tc_commit_2cta_mc(tmem_full, 0x3);
+                if (elect_one()) tc_commit_2cta_mc(&tmem_full[acc], 0x3);
                 __syncwarp();
                 if (lane == 0) G2_STAMP(pair, it_, 2);
-                acc_phase ^= 1;
+                acc_phase ^= 1u << acc;
             }
         }
     } else if (warp >= 4) {
@@ -265,7 +272,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
         const int ew = warp - 4;
         const int quad = warp & 3;            // TMEM lanes [32*quad, 32*quad+32)
         const int cq = ew >> 2;               // column slice of the 256-column tile
-        const uint32_t tmem_empty_leader = mapa_shared(tmem_empty, 0);
+        uint32_t tmem_empty_leader[ACC];
+#pragma unroll
+        for (int a = 0; a < ACC; ++a) tmem_empty_leader[a] = mapa_shared(&tmem_empty[a], 0);
         uint8_t* stg = s_stg + ew * L::STG_BYTES;
         const uint32_t stg_s = smem_u32(stg);
         const float alpha = __fmul_rn(*sA, *sB);
@@ -275,13 +284,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
             int mp, nt;
             g2_tile_coords(tile, m_pairs, n_tiles, mp, nt);
             const int row0 = (mp * 2 + rank) * G2_BM + quad * 32;
-            const int col0 = nt * G2_BN + cq * COLS;
-            mbar_wait(tmem_full, acc_phase);
+            const int col0 = nt * BN + cq * COLS;
+            const int acc = ACC == 1 ? 0 : (it_ & 1);
+            mbar_wait(&tmem_full[acc], (acc_phase >> acc) & 1u);
             tc_fence_after();
             const bool stamp = ew == 0 && rank == 0 && lane == 0;
             if (stamp) G2_STAMP(pair, it_, 3);
             uint32_t r[COLS];
-            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + cq * COLS;
+            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + acc * BN + cq * COLS;
 #pragma unroll
             for (int c = 0; c < COLS / 32; ++c) tmem_ld32(ta + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&r[32 * c]));
             tmem_ld_wait();
@@ -294,10 +304,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
             // in-flight TMA stores of the previous tile (measured with the
             // G2_TIMELINE build: E5-E4 1.06 -> 0.10 us, the whole per-tile bubble).
             if (lane == 0)
-                asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(tmem_empty_leader)
+                asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                                 tmem_empty_leader[acc])
                              : "memory");
             if (stamp) G2_STAMP(pair, it_, 5);
-            acc_phase ^= 1;
+            acc_phase ^= 1u << acc;
             if (!TMA_EPI) {
                 const int64_t row = row0 + lane;
                 if (OUT_BF16) {
@@ -373,12 +384,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
     }
 }
 
-template <bool OUT_BF16, int STAGES, bool TMA_EPI, int EPI_WARPS>
+template <bool OUT_BF16, int STAGES, bool TMA_EPI, int EPI_WARPS, int BN = 256>
 static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
                           const float* sB, void* D, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
                           cudaStream_t st) {
-    using L = G2Layout<STAGES, TMA_EPI, EPI_WARPS>;
-    auto kern = gemm_mxf8_2cta_kernel<OUT_BF16, STAGES, TMA_EPI, EPI_WARPS>;
+    using L = G2Layout<STAGES, TMA_EPI, EPI_WARPS, BN>;
+    auto kern = gemm_mxf8_2cta_kernel<OUT_BF16, STAGES, TMA_EPI, EPI_WARPS, BN>;
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM) != cudaSuccess)
@@ -389,7 +400,7 @@ static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B
     const int64_t sfa_rows = ((M + 127) / 128) * (K / 128) * 2;
     const int64_t sfb_rows = ((N + 127) / 128) * (K / 128) * 2;
     if (!make_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, A, M, K, 128, G2_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, B, N, K, 128, G2_BN / 2, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, B, N, K, 128, BN / 2, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !make_tmap_2d(&tsa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, SFA, sfa_rows, 256, 256, 2, CU_TENSOR_MAP_SWIZZLE_NONE))
         return MOSS_ERR_CUDA;
     tsb = tsa;
@@ -410,7 +421,7 @@ static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return MOSS_ERR_CUDA;
     }
-    const int64_t tiles = (M / (2 * G2_BM)) * (N / G2_BN);
+    const int64_t tiles = (M / (2 * G2_BM)) * (N / BN);
     const int pairs = (int)std::min<int64_t>(tiles, sm_count() / 2);
     kern<<<2 * pairs, (4 + EPI_WARPS) * 32, L::SMEM, st>>>(ta, tb, tsa, tsb, td, D, ldd, sA, sB, (int)M, (int)N, (int)K,
                                                  SFB == nullptr, accumulate);
@@ -418,15 +429,14 @@ static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B
 }
 
 // MOSS_GEMM2_MODE (A/B testing on B200):
-//   2 (default) 6 stages, 8 epilogue warps x 128 columns, TMA-store epilogue
-//   1           5 stages, 16 epilogue warps x 64 columns, TMA-store epilogue
-//   0           6 stages, 16 epilogue warps, direct-store epilogue
+//   2 (default) 256 x 256 pair tiles, 1 TMEM accumulator, 6 stages, 8 epilogue warps, TMA-store epilogue
+//   3           256 x 128 pair tiles, 2 TMEM accumulator stages (epilogue overlapped), 8 stages
 static int gemm2_mode() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("MOSS_GEMM2_MODE");
         v = e ? (e[0] - '0') : 2;
-        if (v < 0 || v > 2) v = 2;
+        if (v != 2 && v != 3) v = 2;
     }
     return v;
 }
@@ -435,20 +445,15 @@ static int gemm2_mode() {
 int launch_gemm2(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
                  const float* sB, void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
                  cudaStream_t st) {
-    if (M % (2 * G2_BM) || N % G2_BN || K % G2_BK) return -1;
+    if (M % (2 * G2_BM) || N % 128 || K % G2_BK) return -1;
     if ((reinterpret_cast<uintptr_t>(D) % 16) || (ldd * (d_dtype == MOSS_BF16 ? 2 : 4)) % 16) return -1;
     const bool bf = d_dtype == MOSS_BF16;
-    switch (gemm2_mode()) {
-        case 1:
-            return bf ? launch_gemm2_t<true, 5, true, 16>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
-                      : launch_gemm2_t<false, 5, true, 16>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
-        case 0:
-            return bf ? launch_gemm2_t<true, 6, false, 16>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
-                      : launch_gemm2_t<false, 6, false, 16>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
-        default:
-            return bf ? launch_gemm2_t<true, 6, true, 8>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
-                      : launch_gemm2_t<false, 6, true, 8>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
-    }
+    const bool n128 = gemm2_mode() == 3 || N % G2_BN != 0;
+    if (n128)
+        return bf ? launch_gemm2_t<true, 8, true, 8, 128>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
+                  : launch_gemm2_t<false, 8, true, 8, 128>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
+    return bf ? launch_gemm2_t<true, 6, true, 8>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
+              : launch_gemm2_t<false, 6, true, 8>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
 }
 
 }  // namespace moss
