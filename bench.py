@@ -411,11 +411,16 @@ def main() -> None:
     issue_ms = (time.perf_counter() - h0) * 1e3
     sleep_cycles = int(issue_ms * 2.5 * 2.0e6)          # ~2.5x the host issue time at ~2 GHz
     _lib.INSTR.start(timing=True)
+    if hasattr(buckets, "timing"):
+        buckets.timing = True
     for _ in range(args.steps):
         torch.cuda._sleep(sleep_cycles)
         step(x)
         torch.cuda.synchronize()
     _lib.INSTR.stop()
+    comm = buckets.comm_summary() if hasattr(buckets, "comm_summary") else None
+    if hasattr(buckets, "timing"):
+        buckets.timing = False
     kern = _lib.INSTR.summary()
     launches = _lib.INSTR.launches // args.steps
     barrier()
@@ -574,6 +579,9 @@ def main() -> None:
                                      "value/ms_per_step from " + ("CUDA-graph replays" if use_graph else "eager steps")},
         "e2e": e2e,
     }
+    if comm is not None:
+        line["collectives"] = {**comm, "note": "bucketed FP32 gradient all-reduce on the comm stream, events per "
+                                                "bucket over the instrumented steps (overlaps backward)"}
     if not llama:
         try:
             cmp = gemm_vs_cublas(dev, T)

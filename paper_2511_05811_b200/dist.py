@@ -66,6 +66,8 @@ class GradBuckets:
                 cur, size = [], 0
         if cur:
             self._make_bucket(cur, size, dev)
+        self.timing = False                 # bench: CUDA events around each bucket's all-reduce
+        self.comm_events: list = []
         self._hooks = []
         for p in self.params:
             if hasattr(p, "moss_layer"):
@@ -131,7 +133,14 @@ class GradBuckets:
             ev.record(torch.cuda.current_stream(b.buf.device))
             self.comm_stream.wait_event(ev)
             with torch.cuda.stream(self.comm_stream):
+                if self.timing:
+                    s = torch.cuda.Event(enable_timing=True)
+                    s.record(self.comm_stream)
                 b.work = dist.all_reduce(b.buf, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+                if self.timing:
+                    e = torch.cuda.Event(enable_timing=True)
+                    e.record(self.comm_stream)
+                    self.comm_events.append((b.buf.numel() * 4, s, e))
         else:
             b.work = dist.all_reduce(b.buf, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
 
@@ -149,6 +158,16 @@ class GradBuckets:
     @property
     def grad_scale(self) -> float:
         return 1.0 / self.world
+
+    def comm_summary(self) -> dict | None:
+        """All-reduce bytes and bus bandwidth 2(n-1)/n x bytes / time (NCCL's busbw) over the timed events."""
+        if not self.comm_events:
+            return None
+        torch.cuda.synchronize()
+        nbytes = sum(b for b, _, _ in self.comm_events)
+        ms = sum(s.elapsed_time(e) for _, s, e in self.comm_events)
+        return {"allreduce_bytes": nbytes, "allreduce_ms": ms, "launches": len(self.comm_events),
+                "busbw_gbs": 2 * (self.world - 1) / self.world * nbytes / (ms / 1e3) / 1e9 if ms > 0 else None}
 
     def total_bytes(self) -> int:
         return sum(b.buf.numel() * 4 for b in self.buckets)
