@@ -28,6 +28,14 @@ def _port():
     return p
 
 
+def _batch(step, rank, world, tokens=512):
+    """Rank's shard of the global batch of ``step`` (the same global batch for any world size)."""
+    g = torch.Generator(device="cuda").manual_seed(1000 + step)
+    full = torch.randn(tokens, 512, device="cuda", dtype=torch.bfloat16, generator=g)
+    n = tokens // world
+    return full[rank * n:(rank + 1) * n].contiguous()
+
+
 def _worker(rank, world, port, mode, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -44,8 +52,7 @@ def _worker(rank, world, port, mode, q):
         opt.grad_scale = ex.grad_scale
         losses = []
         for step in range(4):                                    # includes a rescale at step 3
-            torch.manual_seed(100 + 10 * step + rank)            # per-rank batch shard
-            x = torch.randn(256, 512, device="cuda", dtype=torch.bfloat16)
+            x = _batch(step, rank, world)                        # this rank's shard of the global batch
             ex.reset()
             loss = model(x)
             loss.backward()
@@ -97,3 +104,30 @@ def test_dp_ranks_stay_identical():
     for a, b in zip(res["allreduce"][0][0], res["zero1"][0][0]):
         assert (a == b).mean() > 0.999
     assert np.allclose(res["allreduce"][0][3], res["zero1"][0][3], rtol=1e-3)
+
+
+def test_dp_matches_single_gpu_at_same_global_batch():
+    """2 ranks x 256 tokens vs 1 process x 512 tokens, same global batches:
+    the loss curves agree within 1 % (n-GPU curve within a
+    stated band of the 1-GPU curve).  The only semantic difference is the
+    per-rank activation amax; it perturbs FP8 gradients at the
+    quantization-noise level, which Adam's sign-like early steps turn into
+    different updates of near-zero-gradient weights, so weights are not
+    compared element-wise here (the invariant is rank-to-rank identity, above)."""
+    import numpy as np
+
+    from paper_2511_05811_b200.nn import MossAdamW
+    from paper_2511_05811_b200.workloads import LayerStack
+    torch.manual_seed(0)
+    model = LayerStack(d_model=512, d_ffn=1024, device="cuda", interval=3)
+    opt = MossAdamW(model, lr=1e-3)
+    single = []
+    for step in range(4):
+        opt.zero_grad()
+        loss = model(_batch(step, 0, 1))
+        loss.backward()
+        opt.step()
+        single.append(float(loss))
+    dp = _run("allreduce")
+    dp_loss = (np.array(dp[0][3]) + np.array(dp[1][3])) / 2          # mean of the ranks' shard losses
+    assert np.allclose(dp_loss, single, rtol=1e-2), (dp_loss, single)
