@@ -178,6 +178,15 @@ int moss_swiglu_bwd(const void* dh, const void* gu, void* dgu, float* amax, int6
  * rotated by cos/sin [S_max, hd/2] (f32) at position s */
 int moss_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q, void* k, void* v, int64_t B,
                   int64_t S, int64_t H, int64_t hd, void* stream);
+/* Elementwise glue producers (bf16, f32 math), each writing max|out| to *amax:
+ * mode 0 sum3:   out [T, d] = x[:, 0:d] + x[:, d:2d] + x[:, 2d:3d]   (x [T, 3d])
+ * mode 1 bcast3: out [T, 3d] = [x, x, x]                              (x [T, d])
+ * mode 2 add:    out = x + y
+ * mode 3 scale:  out = x * (*scale)                                    (scale: device f32) */
+int moss_glue(int mode, const void* x, const void* y, const float* scale, void* out, float* amax, int64_t T,
+              int64_t d, void* stream);
+/* *acc = sum x^2 (f32) over n bf16 elements (n % 8 == 0) */
+int moss_sumsq(const void* x, int64_t n, float* acc, void* stream);
 /* Cross entropy of bf16 logits [T, V] (V % 8 == 0) against int64 targets:
  * fwd  lse[t] = logsumexp(x[t, :]) (f32, one read of the row), loss[t] = lse[t] - x[t, y_t]
  * bwd  dlogits = (softmax(x) - onehot(y)) * (*scale), bf16; scale a device f32 (dL/dmean / T) */

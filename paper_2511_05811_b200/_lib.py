@@ -46,6 +46,8 @@ _SIGS = {
     "moss_rope_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
     "moss_transpose_u8": (_I, [_P, _P, _I64, _I64, _P]),
     "moss_cross_entropy_fwd": (_I, [_P, _P, _P, _P, _I64, _I64, _P]),
+    "moss_glue": (_I, [_I, _P, _P, _P, _P, _P, _I64, _I64, _P]),
+    "moss_sumsq": (_I, [_P, _I64, _P, _P]),
     "moss_cross_entropy_bwd": (_I, [_P, _P, _P, _P, _P, _I64, _I64, _P]),
     "moss_quant_per_group": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P, _P]),
     "moss_gemm_pergroup": (_I, [_P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _P]),
@@ -378,3 +380,14 @@ def cross_entropy_bwd(logits, targets, lse, scale, dlogits) -> None:
     with _Span("producer", T * V * 4):
         check(lib().moss_cross_entropy_bwd(logits.data_ptr(), targets.data_ptr(), lse.data_ptr(), scale.data_ptr(),
                                            dlogits.data_ptr(), T, V, stream()), "moss_cross_entropy_bwd")
+
+
+def glue(mode: int, x, out, amax, *, y=None, scale=None, T: int, d: int) -> None:
+    with _Span("producer", T * d * (2 + (4 if mode in (0, 1) else 2) + (2 if mode == 2 else 0))):
+        check(lib().moss_glue(mode, x.data_ptr(), ptr(y), ptr(scale), out.data_ptr(), ptr(amax), T, d, stream()),
+              "moss_glue")
+
+
+def sumsq(x, acc) -> None:
+    with _Span("producer", x.numel() * 2):
+        check(lib().moss_sumsq(x.data_ptr(), x.numel(), acc.data_ptr(), stream()), "moss_sumsq")

@@ -35,6 +35,9 @@ int launch_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void*
 int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
                     float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, cudaStream_t st);
 int launch_transpose_u8(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t st);
+int launch_glue(int mode, const void* x, const void* y, const float* scale, void* out, float* amax, int64_t T,
+                int64_t d, cudaStream_t st);
+int launch_sumsq(const void* x, int64_t n, float* acc, cudaStream_t st);
 int launch_xent_fwd(const void* logits, const int64_t* targets, float* lse, float* loss, int64_t T, int64_t V,
                     cudaStream_t st);
 int launch_xent_bwd(const void* logits, const int64_t* targets, const float* lse, const float* scale, void* dlogits,
@@ -224,6 +227,21 @@ int moss_transpose_u8(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t co
     if (!src || !dst) return MOSS_ERR_ARGUMENT;
     if (!aligned(src, 16) || !aligned(dst, 16) || cols % 16 || rows % 16) return MOSS_ERR_ALIGN;
     return moss::launch_transpose_u8(src, dst, rows, cols, (cudaStream_t)stream);
+}
+
+int moss_glue(int mode, const void* x, const void* y, const float* scale, void* out, float* amax, int64_t T,
+              int64_t d, void* stream) {
+    if (T <= 0 || d <= 0 || d % 8 || mode < 0 || mode > 3) return mode < 0 || mode > 3 ? MOSS_ERR_ARGUMENT : MOSS_ERR_SHAPE;
+    if (!x || !out || (mode == 2 && !y) || (mode == 3 && !scale)) return MOSS_ERR_ARGUMENT;
+    if (!al16(x) || !al16(y) || !al16(out)) return MOSS_ERR_ALIGN;
+    return moss::launch_glue(mode, x, y, scale, out, amax, T, d, (cudaStream_t)stream);
+}
+
+int moss_sumsq(const void* x, int64_t n, float* acc, void* stream) {
+    if (n <= 0 || n % 8) return MOSS_ERR_SHAPE;
+    if (!x || !acc) return MOSS_ERR_ARGUMENT;
+    if (!al16(x)) return MOSS_ERR_ALIGN;
+    return moss::launch_sumsq(x, n, acc, (cudaStream_t)stream);
 }
 
 int moss_cross_entropy_fwd(const void* logits, const int64_t* targets, float* lse, float* loss, int64_t T, int64_t V,

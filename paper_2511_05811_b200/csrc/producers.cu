@@ -443,6 +443,70 @@ __global__ void __launch_bounds__(256) rope_bwd_kernel(const __nv_bfloat16* __re
     block_amax_commit(m, red_u, amax);
 }
 
+// ------------------------------------------------------------------ small glue producers (LayerStack)
+// mode 0: sum3   out [T, d] = a + b + c from x [T, 3d] (column blocks), amax(out)
+// mode 1: bcast3 out [T, 3d] = [x, x, x] from x [T, d],               amax(x)
+// mode 2: add    out [T, d] = x + y,                                  amax(out)
+// mode 3: mse'   out [T, d] = x * (*scale),                           amax(out)   (dL/dy of mean(y^2): scale = 2 g / n)
+__global__ void __launch_bounds__(256) glue_kernel(int mode, const __nv_bfloat16* __restrict__ x,
+                                                   const __nv_bfloat16* __restrict__ y, const float* __restrict__ scale,
+                                                   __nv_bfloat16* __restrict__ out, uint32_t* amax, int64_t T, int d) {
+    __shared__ uint32_t red_u[8];
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    uint32_t m = 0;
+    const float sc = mode == 3 ? *scale : 0.f;
+    if (c < d) {
+        for (int64_t t = blockIdx.y; t < T; t += gridDim.y) {
+            float a[8], b[8];
+            if (mode == 0) {
+                const __nv_bfloat16* r = x + t * 3 * d + c;
+                float e[8];
+                bf16x8_load(r, a);
+                bf16x8_load(r + d, b);
+                bf16x8_load(r + 2 * d, e);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) a[k] += b[k] + e[k];
+            } else {
+                bf16x8_load(x + t * d + c, a);
+                if (mode == 2) {
+                    bf16x8_load(y + t * d + c, b);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) a[k] += b[k];
+                } else if (mode == 3) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) a[k] *= sc;
+                }
+            }
+            const uint4 o = bf16x8_pack(a);
+            if (mode == 1) {
+                __nv_bfloat16* r = out + t * 3 * d + c;
+                *reinterpret_cast<uint4*>(r) = o;
+                *reinterpret_cast<uint4*>(r + d) = o;
+                *reinterpret_cast<uint4*>(r + 2 * d) = o;
+            } else {
+                *reinterpret_cast<uint4*>(out + t * d + c) = o;
+            }
+            m = max(m, absmax_bits_bf16(o));
+        }
+    }
+    block_amax_commit(m, red_u, amax);
+}
+
+// sum of squares of a bf16 tensor in f32 -> *acc (atomicAdd per CTA; zeroed by the launcher)
+__global__ void __launch_bounds__(256) sumsq_kernel(const __nv_bfloat16* __restrict__ x, int64_t nvec,
+                                                    float* __restrict__ acc) {
+    __shared__ float red[8];
+    float ssum = 0.f;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
+        float v[8];
+        bf16x8_load(x + i * 8, v);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ssum = fmaf(v[k], v[k], ssum);
+    }
+    ssum = block_sum<256>(ssum, red);
+    if (threadIdx.x == 0) atomicAdd(acc, ssum);
+}
+
 // ------------------------------------------------------------------ cross entropy (LM head)
 // forward: one CTA per row of bf16 logits [T, V]: online max / sum-exp in f32
 // (one read of the row), lse[t] = max + log(sum), loss[t] = lse[t] - x[t, y_t]
@@ -636,6 +700,25 @@ int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float*
     rope_bwd_kernel<<<dim3((unsigned)(B * S), (unsigned)((H * (hd / 8) + 255) / 256)), 256, 0, st>>>(
         (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv, cosv, sinv,
         (__nv_bfloat16*)dqkv, reinterpret_cast<uint32_t*>(amax), (int)B, (int)S, (int)H, (int)hd);
+    return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+}
+
+int launch_glue(int mode, const void* x, const void* y, const float* scale, void* out, float* amax, int64_t T,
+                int64_t d, cudaStream_t st) {
+    if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
+    const int64_t gx = (d / 8 + 255) / 256;
+    const int64_t gy = std::min<int64_t>(T, std::max<int64_t>(1, (int64_t)sm_count() * 16 / gx));
+    glue_kernel<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, st>>>(mode, (const __nv_bfloat16*)x,
+                                                                 (const __nv_bfloat16*)y, scale, (__nv_bfloat16*)out,
+                                                                 reinterpret_cast<uint32_t*>(amax), T, (int)d);
+    return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+}
+
+int launch_sumsq(const void* x, int64_t n, float* acc, cudaStream_t st) {
+    if (cudaMemsetAsync(acc, 0, 4, st) != cudaSuccess) return MOSS_ERR_CUDA;
+    const int64_t nvec = n / 8;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nvec + 255) / 256, (int64_t)sm_count() * 8));
+    sumsq_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, nvec, acc);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 

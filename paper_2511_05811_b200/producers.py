@@ -19,7 +19,8 @@ import torch
 
 from . import _lib
 
-__all__ = ["RMSNormFn", "AddRMSNormFn", "SwiGLUFn", "RopeQKVFn", "CrossEntropyFn"]
+__all__ = ["RMSNormFn", "AddRMSNormFn", "SwiGLUFn", "RopeQKVFn", "CrossEntropyFn", "Sum3Fn", "AddFn",
+           "MeanSquareFn"]
 
 
 def _c2(t: torch.Tensor, d: int) -> torch.Tensor:
@@ -169,3 +170,69 @@ class CrossEntropyFn(torch.autograd.Function):
         d = torch.empty_like(lg)
         _lib.cross_entropy_bwd(lg, tg, lse, scale, d)
         return d.view(ctx.shape), None
+
+
+# ---------------------------------------------------------------- glue of the LayerStack benchmark workload
+class Sum3Fn(torch.autograd.Function):
+    """qkv [T, 3d] -> (q + k + v, amax); backward broadcasts da to [da, da, da]
+    with amax for ``consumer`` (the qkv layer)."""
+
+    @staticmethod
+    def forward(ctx, qkv, consumer):
+        d3 = qkv.shape[-1]
+        x = _c2(qkv, d3)
+        out = torch.empty(x.shape[0], d3 // 3, dtype=x.dtype, device=x.device)
+        amax = torch.empty(1, dtype=torch.float32, device=x.device)
+        _lib.glue(0, x, out, amax, T=x.shape[0], d=d3 // 3)
+        ctx.consumer, ctx.shape = consumer, qkv.shape
+        ctx.mark_non_differentiable(amax)
+        return out.view(*qkv.shape[:-1], d3 // 3), amax
+
+    @staticmethod
+    def backward(ctx, da, _):
+        d = ctx.shape[-1] // 3
+        da2 = _c2(da, d)
+        out = torch.empty(da2.shape[0], 3 * d, dtype=da2.dtype, device=da2.device)
+        _lib.glue(1, da2, out, _amax_buf(ctx.consumer, out), T=da2.shape[0], d=d)
+        return out.view(ctx.shape), None
+
+
+class AddFn(torch.autograd.Function):
+    """(x + y, amax(x + y)) in one pass; the gradient passes to both inputs."""
+
+    @staticmethod
+    def forward(ctx, x, y):
+        d = x.shape[-1]
+        x2, y2 = _c2(x, d), _c2(y, d)
+        out = torch.empty_like(x2)
+        amax = torch.empty(1, dtype=torch.float32, device=x.device)
+        _lib.glue(2, x2, out, amax, y=y2, T=x2.shape[0], d=d)
+        ctx.mark_non_differentiable(amax)
+        return out.view(x.shape), amax
+
+    @staticmethod
+    def backward(ctx, g, _):
+        return g, g
+
+
+class MeanSquareFn(torch.autograd.Function):
+    """mean(y^2) in f32 over a bf16 tensor; backward dy = 2 y g / n (bf16) with
+    amax for ``consumer`` (the layer that produced y)."""
+
+    @staticmethod
+    def forward(ctx, y, consumer):
+        d = y.shape[-1]
+        y2 = _c2(y, d)
+        acc = torch.empty(1, dtype=torch.float32, device=y.device)
+        _lib.sumsq(y2, acc)
+        ctx.save_for_backward(y2)
+        ctx.consumer, ctx.shape = consumer, y.shape
+        return (acc / y2.numel()).reshape(())
+
+    @staticmethod
+    def backward(ctx, g):
+        (y2,) = ctx.saved_tensors
+        scale = (g.float() * (2.0 / y2.numel())).reshape(1).contiguous()
+        dy = torch.empty_like(y2)
+        _lib.glue(3, y2, dy, _amax_buf(ctx.consumer, dy), scale=scale, T=y2.shape[0], d=y2.shape[1])
+        return dy.view(ctx.shape), None

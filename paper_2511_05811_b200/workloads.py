@@ -9,9 +9,11 @@ backward gradient:
     qkv = QKV(x); a = q + k + v              (stand-in for attention mixing)
     r = x + O(a); h = silu(gate(r)) * up(r); y = down(h); loss = mean(y^2)
 
-The SwiGLU is the producer kernel (producers.SwiGLUFn): it hands amax(h) to
-the down projection's quantizer and amax(dgu) to gate_up's backward, as in
-the Llama decoder.
+The glue ops are producer kernels (producers.py) as in the Llama decoder:
+each writes the amax of the tensor it makes, so the quantizers of a/r/h (fwd)
+and of the qkv/gate_up/down output-gradients run in producer-amax mode (one
+read, no reduction).  Only x (the step's input) and o's output-gradient (the
+gate_up dgrad GEMM's output) are quantized with the in-kernel amax.
 
 One step = forward + backward (FP8 fwd/dgrad/wgrad for every linear, each
 input and gradient two-level quantized row- and column-wise) + MossAdamW
@@ -25,7 +27,7 @@ import torch
 from torch import nn
 
 from .nn import MossLinear
-from .producers import SwiGLUFn
+from .producers import AddFn, MeanSquareFn, Sum3Fn, SwiGLUFn
 
 LLAMA7B_SHAPES = {"qkv": (4096, 12288), "o": (4096, 4096), "gate_up": (4096, 22016), "down": (11008, 4096)}
 
@@ -40,12 +42,10 @@ class LayerStack(nn.Module):
         self.down = MossLinear(d_ffn, d_model, device=device, interval=interval)
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
-        q, k, v = self.qkv(x).split(self.d, dim=-1)
-        a = q + k + v
-        r = x + self.o(a)
-        h, am = SwiGLUFn.apply(self.gate_up(r), self.gate_up)
-        y = self.down(h, am)
-        return (y.float() ** 2).mean()
+        a, am = Sum3Fn.apply(self.qkv(x), self.qkv)              # a = q + k + v
+        r, am = AddFn.apply(x, self.o(a, am))                     # r = x + O(a)
+        h, am = SwiGLUFn.apply(self.gate_up(r, am), self.gate_up)
+        return MeanSquareFn.apply(self.down(h, am), self.down)    # mean(y^2)
 
     def gemm_flops_per_token(self) -> int:
         return 6 * sum(m.in_features * m.out_features for m in (self.qkv, self.o, self.gate_up, self.down))

@@ -177,3 +177,42 @@ def test_cross_entropy_fused(T, V):
     (loss * 2.0).backward()
     (ref * 2.0).backward()
     close_bf16(logits.grad, lf.grad, rtol=2 ** -7, atol=1e-8)
+
+
+@pytest.mark.parametrize("T,d", [(1, 8), (333, 4096), (4096, 4096), (64, 11008)])
+def test_glue_kernels(T, d):
+    """LayerStack glue (moss_glue / moss_sumsq) vs torch fp32, amax exact."""
+    from paper_2511_05811_b200.producers import AddFn, MeanSquareFn, Sum3Fn
+    torch.manual_seed(T + d)
+    qkv = torch.randn(T, 3 * d, device="cuda", dtype=torch.bfloat16, requires_grad=True)
+    a, am = Sum3Fn.apply(qkv, None)
+    ref = qkv.detach().float().view(T, 3, d).sum(1)
+    close_bf16(a, ref, rtol=2 ** -7, atol=2e-2)
+    exact_amax(am, a)
+    x = torch.randn(T, d, device="cuda", dtype=torch.bfloat16, requires_grad=True)
+    r, am = AddFn.apply(x, a)
+    close_bf16(r, x.detach().float() + a.detach().float(), atol=2e-2)
+    exact_amax(am, r)
+    lin = mnn.MossLinear(32, 32, device="cuda")
+    loss = MeanSquareFn.apply(r, lin)
+    rf = r.detach().float()
+    assert abs(float(loss) - float((rf ** 2).mean())) <= 1e-5 * float((rf ** 2).mean()) + 1e-12
+    loss.backward()
+    # d loss / d r = 2 r / n reaches x unchanged and qkv broadcast to its three blocks
+    g = (2.0 / rf.numel()) * rf
+    close_bf16(x.grad, g, atol=1e-12)
+    exact_amax(lin.dy_amax, x.grad)
+    gq = qkv.grad.view(T, 3, d)
+    assert torch.equal(gq[:, 0], x.grad) and torch.equal(gq[:, 1], x.grad) and torch.equal(gq[:, 2], x.grad)
+
+
+def test_glue_dy_amax_reaches_consumer():
+    """Sum3Fn backward writes amax(dqkv) into the consumer's dy_amax buffer."""
+    from paper_2511_05811_b200.producers import Sum3Fn
+    T, d = 256, 512
+    lin = mnn.MossLinear(d, 3 * d, device="cuda")
+    qkv = torch.randn(T, 3 * d, device="cuda", dtype=torch.bfloat16, requires_grad=True)
+    a, _ = Sum3Fn.apply(qkv, lin)
+    da = torch.randn(T, d, device="cuda", dtype=torch.bfloat16)
+    a.backward(da)
+    exact_amax(lin.dy_amax, da)
