@@ -79,19 +79,32 @@ struct G2Layout {
     static constexpr uint32_t TMEM_COLS = 512;                 // ACC * BN = 256 accumulator + SF columns
 };
 
-// Tile raster: groups of G2_GROUP_M m-pairs walked n-major, so the ~74
-// concurrently running pair tiles share a 2048-row A panel and a few B panels
-// (both L2-resident); a plain m-major walk re-read all of A from DRAM for every
-// n column on tall problems (12288 x 4096 x 8192: 49 % DRAM, 4x the bytes).
-constexpr int G2_GROUP_M = 8;
-__device__ __forceinline__ void g2_tile_coords(int tile, int m_pairs, int n_tiles, int& mp, int& nt) {
-    const int group = G2_GROUP_M * n_tiles;
-    const int gi = tile / group;
-    const int first = gi * G2_GROUP_M;
-    const int gm = min(m_pairs - first, G2_GROUP_M);
-    const int r = tile - gi * group;
-    mp = first + r % gm;
-    nt = r / gm;
+// Tile raster: groups of |raster| m-pairs (raster > 0) walked n-major, or of
+// |raster| n-tiles (raster < 0) walked m-major.  The ~74 concurrently running
+// pair tiles then share one resident panel of the grouped operand (L2) while
+// the other operand streams; the host (g2_raster) sizes the group so the
+// resident panel fits the L2 budget and picks the orientation with the fewest
+// DRAM bytes.  (A plain m-major walk re-read all of A for every n column on
+// tall problems: 12288 x 4096 x 8192 ran at 49 % DRAM with 4x the bytes.)
+__device__ __forceinline__ void g2_tile_coords(int tile, int m_pairs, int n_tiles, int raster, int& mp, int& nt) {
+    if (raster > 0) {
+        const int group = raster * n_tiles;
+        const int gi = tile / group;
+        const int first = gi * raster;
+        const int gm = min(m_pairs - first, raster);
+        const int r = tile - gi * group;
+        mp = first + r % gm;
+        nt = r / gm;
+    } else {
+        const int g = -raster;
+        const int group = g * m_pairs;
+        const int gi = tile / group;
+        const int first = gi * g;
+        const int gn = min(n_tiles - first, g);
+        const int r = tile - gi * group;
+        nt = first + r % gn;
+        mp = r / gn;
+    }
 }
 
 // SF buffers are viewed as [bytes/256, 256] u8 tensors: one 512 B chunk = box {256, 2}
@@ -103,7 +116,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                           const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
                           const __grid_constant__ CUtensorMap tmD, void* __restrict__ D, int64_t ldd,
                           const float* __restrict__ sA, const float* __restrict__ sB, int M, int N, int K,
-                          int unit_b, int accumulate) {
+                          int unit_b, int accumulate, int raster) {
     using L = G2Layout<STAGES, TMA_EPI, EPI_WARPS, BN>;
     constexpr int ACC = L::ACC;
     constexpr int COLS = BN / (EPI_WARPS / 4);      // accumulator columns per epilogue warp
@@ -168,7 +181,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
         uint32_t phase = 0;
         for (int tile = pair; tile < num_tiles; tile += npairs) {
             int mp, nt;
-            g2_tile_coords(tile, m_pairs, n_tiles, mp, nt);
+            g2_tile_coords(tile, m_pairs, n_tiles, raster, mp, nt);
             const int mb = mp * 2 + rank;                       // this CTA's 128-row block of A
             const int n0 = nt * BN + rank * (BN / 2);           // this CTA's half of B
             for (int kb = 0; kb < kblocks; ++kb) {
@@ -282,7 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
         int it_ = 0;
         for (int tile = pair; tile < num_tiles; tile += npairs, ++it_) {
             int mp, nt;
-            g2_tile_coords(tile, m_pairs, n_tiles, mp, nt);
+            g2_tile_coords(tile, m_pairs, n_tiles, raster, mp, nt);
             const int row0 = (mp * 2 + rank) * G2_BM + quad * 32;
             const int col0 = nt * BN + cq * COLS;
             const int acc = ACC == 1 ? 0 : (it_ & 1);
@@ -384,6 +397,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
     }
 }
 
+// Raster choice (host): keep a panel of one operand L2-resident and stream the
+// other.  Grouping m-pairs re-reads B once per group, grouping n-tiles re-reads
+// A once per group; the group is the largest whose panel fits the budget
+// (MOSS_GEMM2_L2MB, default 80 MB of the 126 MB L2) and the orientation with
+// the fewer modelled DRAM bytes wins.  Measured over the 12 LayerStack GEMMs
+// (ncu dram bytes per launch): fixed 8-m-pair groups (MOSS_GEMM2_L2MB=0) 437 MB,
+// budget 40 -> 376, 80 -> 366, 120 -> 514 (the panel no longer survives a wave
+// of streamed tiles), every launch at 80 at or below the fixed raster.  A
+// budget that also charges one wave of streamed panels was tried and was worse
+// (430 MB: it falls back to tiny groups on K = 22016 where concurrent tiles
+// still share panels within a wave).
+static int g2_raster(int64_t m_pairs, int64_t n_tiles, int BN, int64_t K) {
+    static int64_t budget = -1;
+    if (budget < 0) {
+        const char* e = getenv("MOSS_GEMM2_L2MB");
+        budget = (e ? atoll(e) : 80) << 20;
+    }
+    if (budget == 0) return 8;
+    const int64_t a_pair = 2 * G2_BM * K, b_tile = (int64_t)BN * K;       // one panel (all of K)
+    const int64_t gm = std::max<int64_t>(1, std::min<int64_t>(m_pairs, budget / a_pair));
+    const int64_t gn = std::max<int64_t>(1, std::min<int64_t>(n_tiles, budget / b_tile));
+    const int64_t bytes_m = m_pairs * a_pair + ((m_pairs + gm - 1) / gm) * n_tiles * b_tile;
+    const int64_t bytes_n = n_tiles * b_tile + ((n_tiles + gn - 1) / gn) * m_pairs * a_pair;
+    return bytes_m <= bytes_n ? (int)gm : -(int)gn;
+}
+
 template <bool OUT_BF16, int STAGES, bool TMA_EPI, int EPI_WARPS, int BN = 256>
 static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
                           const float* sB, void* D, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
@@ -423,8 +462,9 @@ static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B
     }
     const int64_t tiles = (M / (2 * G2_BM)) * (N / BN);
     const int pairs = (int)std::min<int64_t>(tiles, sm_count() / 2);
+    const int raster = g2_raster(M / (2 * G2_BM), N / BN, BN, K);
     kern<<<2 * pairs, (4 + EPI_WARPS) * 32, L::SMEM, st>>>(ta, tb, tsa, tsb, td, D, ldd, sA, sB, (int)M, (int)N, (int)K,
-                                                 SFB == nullptr, accumulate);
+                                                 SFB == nullptr, accumulate, raster);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 
