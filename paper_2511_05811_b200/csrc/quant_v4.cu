@@ -117,10 +117,19 @@ __device__ __forceinline__ float q4_unpack(const uint32_t (&w)[NP], float (&lo)[
         lo[i] = __uint_as_float(w[i] * 65536u + 0x80000000u);
         hi[i] = __uint_as_float((w[i] & 0xFFFF0000u) ^ 0x80000000u);
     }
-    float bm = 0.f;
+    // block max |x| on the packed words: one max.xorsign.abs.bf16x2 per pair of
+    // words (magnitude = max(|a|, |b|) per half, exact; the sign bit is masked)
+    uint32_t t[NP];
 #pragma unroll
-    for (int i = 0; i < NP; ++i) bm = fmaxf(bm, fmaxf(fabsf(lo[i]), fabsf(hi[i])));
-    return bm;
+    for (int i = 0; i < NP; ++i) t[i] = w[i];
+#pragma unroll
+    for (int step = 1; step < NP; step *= 2) {
+#pragma unroll
+        for (int i = 0; i + step < NP; i += 2 * step)
+            asm("max.xorsign.abs.bf16x2 %0, %1, %2;" : "=r"(t[i]) : "r"(t[i]), "r"(t[i + step]));
+    }
+    const uint32_t mm = t[0] & 0x7FFF7FFFu;
+    return fmaxf(__uint_as_float(mm << 16), __uint_as_float(mm & 0xFFFF0000u));
 }
 
 // E8M0 code of a block with max |x| = bm; e = code - 127, eff = g * 2^e.
