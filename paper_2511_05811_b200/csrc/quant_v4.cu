@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
     // row pass: thread (rr, kb0) owns blocks (rr, kb0) and (rr, kb0 + 2);
     // col pass: thread (rb, cp) owns the 32-row blocks rb of columns 2cp, 2cp+1.
     // (A 512-thread variant with half-blocks per thread measured 25 % slower:
-    // the kernel is ALU-issue bound and the split adds per-block work.)
+    // the kernel is latency-bound at 16 warps/SM and the split adds per-block work.)
     // All smem offsets are hoisted out of the tile loop: with the SWIZZLE_128B
     // layouts the per-access offset is a per-thread base XOR a compile-time
     // chunk index (the base has zero bits 4-6).
