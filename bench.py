@@ -256,7 +256,8 @@ def llama7b_submeasure() -> dict:
         d = json.loads(out.stdout.strip().splitlines()[-1])
         return {"tokens_per_s": d["value"], "ms_per_step": d["ms_per_step"], "steps": d["steps"],
                 "config": d["config"]["workload"], "gemm_tflops_in_step": d["roofline"]["achieved"],
-                "gemm_share_of_step": d["roofline"]["share_of_step"], "clocks": d["clocks"]}
+                "gemm_share_of_step": d["roofline"]["share_of_step"], "clocks": d["clocks"],
+                "peak_allocated_gb": d.get("memory", {}).get("peak_allocated_gb")}
     except Exception as ex:  # noqa: BLE001 - a sub-measurement must not sink the bench line
         return {"error": str(ex)[:200]}
 
@@ -501,6 +502,9 @@ def main() -> None:
                "ms_per_step": ms_e2e,
                "pipeline": "pinned H2D of step i+1 on a copy stream overlapped with step i; per-step loss D2H async"}
 
+    # peak device memory of the training run (weights, optimizer state, FP8 copies,
+    # the stashed FP8 activation codes, graph pool), before any side measurement
+    peak_gb = torch.cuda.max_memory_allocated(dev) / 1e9
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
         return
@@ -578,6 +582,8 @@ def main() -> None:
                                      "(device sleep ahead of each step: no host gaps inside the events); "
                                      "value/ms_per_step from " + ("CUDA-graph replays" if use_graph else "eager steps")},
         "e2e": e2e,
+        "memory": {"peak_allocated_gb": peak_gb,
+                   "note": "torch.cuda.max_memory_allocated over warm-up, instrumented pass and timed steps"},
     }
     if comm is not None:
         line["collectives"] = {**comm, "note": "bucketed FP32 gradient all-reduce on the comm stream, events per "
