@@ -193,6 +193,9 @@ class MossLinear(nn.Module):
         # backward of the op that consumes our output, read by our backward)
         self.register_buffer("dy_amax", torch.zeros(1, dtype=torch.float32, device=device), persistent=False)
         self._dy_amax_ptr = None
+        # set by zero.Zero1 when this weight's FP8 codes arrive by an async
+        # all-gather: a callable that makes the current stream wait for them
+        self.fp8_pending = None
 
     def offer_dy_amax(self, dy: torch.Tensor) -> torch.Tensor:
         """Called by the producer of dY before it launches: returns the amax
@@ -232,6 +235,9 @@ class MossLinear(nn.Module):
     def forward(self, x: torch.Tensor, amax: torch.Tensor | None = None) -> torch.Tensor:
         if self.schedule is None:
             self.init_fp8()
+        if self.fp8_pending is not None:
+            pending, self.fp8_pending = self.fp8_pending, None
+            pending()
         return MossLinearFunction.apply(x, self.weight, self, amax)
 
     def extra_repr(self) -> str:

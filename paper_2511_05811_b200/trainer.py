@@ -87,4 +87,6 @@ def train(model: LlamaModel, data: MarkovTokens, *, steps: int, batch: int, seq:
         if not math.isfinite(lv) or lv > divergence_threshold:
             raise TrainDivergedError(f"loss {lv} at step {step}")
         log.loss.append(lv)
+    if hasattr(buckets, "sync"):
+        buckets.sync()                               # land the last step's overlapped FP8 all-gathers
     return log

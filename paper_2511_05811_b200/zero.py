@@ -16,7 +16,11 @@ MossLinear weight W (the FP8 linears, ~96 % of a Llama's parameters):
   * the E4M3 codes of every slice are all-gathered (1 byte per parameter on
     the wire, not 4: the FP8 all-gather) into the codes buffer the forward
     GEMMs read, and each rank rebuilds the dgrad operand W_fp8^T locally with
-    a byte transpose (per-tensor codes commute with the transpose);
+    a byte transpose (per-tensor codes commute with the transpose).  With
+    ``overlap_gather`` (default) the all-gathers are issued asynchronously in
+    forward layer order at the end of ``step`` and each MossLinear waits for
+    its bucket's gather (and transposes) only when the next forward reaches
+    it, so the exchange overlaps the preceding layers' forward compute;
   * scales: s_t advances on the host identically on every rank
     (autoscale.py:71-79, O(1), no data); a rescale step (autoscale.py:86-96)
     max-all-reduces the per-slice amax of W' (one small collective), snaps
@@ -88,8 +92,9 @@ class Zero1:
     dist.GradBuckets (``reset``, ``finish``, ``grad_scale``) plus ``step``,
     which replaces ``opt.step()``."""
 
-    def __init__(self, opt: MossAdamW, bucket_mb: float = 64.0, group=None):
+    def __init__(self, opt: MossAdamW, bucket_mb: float = 64.0, group=None, overlap_gather: bool = True):
         self.opt = opt
+        self.overlap_gather = overlap_gather
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -235,6 +240,7 @@ class Zero1:
     # ------------------------------------------------------------------ step
     @torch.no_grad()
     def step(self, lr: float | None = None) -> None:
+        self.sync()                              # codes of the previous step must have landed
         opt = self.opt
         rescale = opt.prepare(lr)
         opt.launch(rescale)                      # replicated parameters (sharded ones are skipped)
@@ -274,13 +280,38 @@ class Zero1:
         opt._rescale_pending = False
 
     def _gather(self) -> None:
-        """FP8 all-gather of every bucket's codes, then the local W_fp8^T rebuild."""
+        """FP8 all-gather of every bucket's codes, then the local W_fp8^T rebuild
+        (deferred to each layer's next forward when ``overlap_gather``)."""
+        if self.overlap_gather and dist.is_initialized():
+            # (also at world 1, where the in-place gather is a copy onto itself:
+            # keeps this path exercised by the single-GPU tests)
+            for b in reversed(self.buckets):      # buckets were built in backward order
+                S = b.length // self.world
+                work = dist.all_gather_into_tensor(b.codes, b.codes[self.rank * S:(self.rank + 1) * S],
+                                                   group=self.group, async_op=True)
+                for p in b.params:
+                    p.moss_layer.fp8_pending = self._arrival(work, p.moss_layer)
+            return
         if self.world > 1:
             for b in self.buckets:
                 S = b.length // self.world
                 dist.all_gather_into_tensor(b.codes, b.codes[self.rank * S:(self.rank + 1) * S], group=self.group)
         for p in self.moss:
             self._transpose(p.moss_layer)
+
+    def _arrival(self, work, layer):
+        def arrived() -> None:
+            work.wait()                           # NCCL: a stream dependency, no host block
+            self._transpose(layer)
+        return arrived
+
+    def sync(self) -> None:
+        """Complete every pending FP8 all-gather (codes and transposes current)."""
+        for p in self.moss:
+            layer = p.moss_layer
+            if layer.fp8_pending is not None:
+                pending, layer.fp8_pending = layer.fp8_pending, None
+                pending()
 
     def state_bytes(self) -> int:
         """Optimizer-state bytes held by this rank for the MOSS weights (m, v slices)."""

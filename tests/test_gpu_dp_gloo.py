@@ -63,6 +63,8 @@ def _worker(rank, world, port, mode, q):
                 opt.step()
             opt.check("dp")
             losses.append(float(loss))
+        if mode == "zero1":
+            ex.sync()                                            # land the overlapped FP8 all-gathers
         mods = [model.qkv, model.o, model.gate_up, model.down]
         q.put((rank, [m.w_fp8.cpu().numpy() for m in mods], [m.w_fp8_t.cpu().numpy() for m in mods],
                [float(m.w_scale) for m in mods], losses))

@@ -45,6 +45,7 @@ class _Layer:
         self.w_fp8_t = self.w_fp8.t().contiguous()
         self.w_scale = torch.tensor([np.float32(s0)])
         self.w_amax = torch.zeros(1)
+        self.fp8_pending = None        # set by Zero1's overlapped all-gather
         self._buffers = {}
 
     def __setattr__(self, k, v):
@@ -134,7 +135,7 @@ def _grads(rank, step):
     return [torch.randn(s, generator=g) * 1e-2 for s in SHAPES]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, overlap=True):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -142,7 +143,7 @@ def _worker(rank, world, port, q):
         import paper_2511_05811_b200.zero as Z
         layers = [_Layer(o, i, seed=k) for k, (o, i) in enumerate(SHAPES)]
         opt = _StubOpt(layers)
-        z = Z.Zero1(opt, bucket_mb=0.02)              # ~5k floats per bucket: several buckets
+        z = Z.Zero1(opt, bucket_mb=0.02, overlap_gather=overlap)   # ~5k floats per bucket: several buckets
         assert len(z.buckets) >= 2
         # every part is 256-aligned inside its parameter, slices tile each bucket
         for b in z.buckets:
@@ -161,6 +162,11 @@ def _worker(rank, world, port, q):
                 lay.weight.grad_ready_hook(lay.weight)
             z.finish()
             z.step()
+            if overlap:
+                # async all-gathers are in flight until a forward (or sync) consumes them
+                assert all(lay.fp8_pending is not None for lay in layers)
+        z.sync()
+        assert all(lay.fp8_pending is None for lay in layers)
         # numpy copies: torch tensors in a spawn queue die with the child's shared-memory handles
         q.put((rank, [(lay.w_fp8.numpy().copy(), lay.w_fp8_t.numpy().copy(), float(lay.w_scale),
                        lay.schedule.s_t, lay.schedule.last_rescale_step) for lay in layers], "", z.state_bytes()))
@@ -199,12 +205,12 @@ def _replicated_reference(world):
     return layers
 
 
-@pytest.mark.parametrize("world", [2])
-def test_zero1_matches_replicated_world2(world):
+@pytest.mark.parametrize("world,overlap", [(2, True), (2, False)])
+def test_zero1_matches_replicated_world2(world, overlap):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, overlap)) for r in range(world)]
     for p in procs:
         p.start()
     out = {}
