@@ -1,3 +1,6 @@
+"""configs[2] diagnostic: the ~125M Llama on Markov tokens, bf16 linears vs MOSS FP8
+(fwd+bwd) vs MOSS FP8 forward with full-precision backward, two learning rates;
+smoothed final / mid-run losses.  argv: steps."""
 import sys, os, numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2511_05811_b200 import llama as L

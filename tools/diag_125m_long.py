@@ -1,3 +1,5 @@
+"""configs[2] long-horizon band: ~125M Llama, bf16 vs MOSS FP8 linears, one lr.
+argv: steps lr warmup [batch]."""
 import sys, os, numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2511_05811_b200 import llama as L

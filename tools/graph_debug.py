@@ -1,3 +1,5 @@
+"""CUDA-graph capture checks of MossLinear / MossAdamW pieces one at a time (which
+op breaks capture).  Diagnostic only."""
 import sys, os, traceback
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

@@ -1,3 +1,5 @@
+"""torch-profiler kernel table of the Llama-2-7B-shape step (argv: layers; seq 4096,
+batch 1): shares of K2, K3, K1, producers, SDPA, head."""
 import sys, os, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2511_05811_b200.llama import LLAMA2_7B, LlamaConfig, LlamaModel

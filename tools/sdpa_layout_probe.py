@@ -1,3 +1,5 @@
+"""Strides of the SDPA output for [B,S,H,hd]-viewed vs contiguous [B,H,S,hd]
+inputs: does O-projection input need a transpose copy?  Diagnostic only."""
 import torch, torch.nn.functional as F
 B,S,H,hd = 1, 4096, 32, 128
 qkv = torch.randn(B, S, 3, H, hd, device="cuda", dtype=torch.bfloat16, requires_grad=True)
