@@ -127,6 +127,14 @@ typedef struct {
     float grad_scale; /* g is multiplied by this first (DP averaging, grad accumulation); 1 = none */
 } moss_adam_params;
 
+/* moss_gemm_mxf8 with B given as stored [K, N] row-major (N contiguous) and unit
+ * B scales: the dgrad product dX = dY W reads the per-tensor E4M3 weight codes
+ * W [out = K, in = N] directly (MN-major tcgen05 operand) — no transposed copy
+ * of W is kept (replaces the W^T operand of gemm.py:115-129 in the backward).
+ * M % 256, N % 256, K % 128. */
+int moss_gemm_mxf8_bkn(const uint8_t* A, const uint8_t* SFA, const uint8_t* B_kn, const float* sA, const float* sB,
+                       void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, void* stream);
+
 /* K3: fused AdamW + automatic scaling + FP8 weight copy
  * (adamw_step optim.py:78-106, then _quantize_weight train.py:113-118 at the
  * advanced scale s_{t+1} = s_t + eta/448, autoscale.py:71-79).

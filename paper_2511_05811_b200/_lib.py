@@ -47,6 +47,7 @@ _SIGS = {
     "moss_transpose_u8": (_I, [_P, _P, _I64, _I64, _P]),
     "moss_cross_entropy_fwd": (_I, [_P, _P, _P, _P, _I64, _I64, _P]),
     "moss_glue": (_I, [_I, _P, _P, _P, _P, _P, _I64, _I64, _P]),
+    "moss_gemm_mxf8_bkn": (_I, [_P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _P]),
     "moss_sumsq": (_I, [_P, _I64, _P, _P]),
     "moss_cross_entropy_bwd": (_I, [_P, _P, _P, _P, _P, _I64, _I64, _P]),
     "moss_quant_per_group": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P, _P]),
@@ -267,6 +268,16 @@ def gemm(a, sfa, b, sfb, s_a, s_b, d, *, accumulate: bool = False) -> None:
                                    s_b.data_ptr(), d.data_ptr(), dtype_code(d), d.stride(0), m, n, k,
                                    int(accumulate), stream()),
               "moss_gemm_mxf8")
+
+
+def gemm_bkn(a, sfa, b_kn, s_a, s_b, d) -> None:
+    """D = A B with B = b_kn [K, N] row-major (the weight as stored), unit B scales."""
+    m, k = a.shape
+    n = b_kn.shape[1]
+    with _Span("gemm", 2.0 * m * n * k):
+        check(lib().moss_gemm_mxf8_bkn(a.data_ptr(), sfa.data_ptr(), b_kn.data_ptr(), s_a.data_ptr(), s_b.data_ptr(),
+                                       d.data_ptr(), dtype_code(d), d.stride(0), m, n, k, stream()),
+              "moss_gemm_mxf8_bkn")
 
 
 def adamw_fp8_dev(w, g, m, v, rows: int, cols: int, p_dev: int, enc_dev: int | None, flags: FlagWord, *,

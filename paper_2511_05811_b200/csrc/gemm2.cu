@@ -110,7 +110,11 @@ __device__ __forceinline__ void g2_tile_coords(int tile, int m_pairs, int n_tile
 // SF buffers are viewed as [bytes/256, 256] u8 tensors: one 512 B chunk = box {256, 2}
 __device__ __forceinline__ int sf_row_of_chunk(int64_t chunk) { return (int)(chunk * 2); }
 
-template <bool OUT_BF16, int STAGES, bool TMA_EPI, int EPI_WARPS, int BN>
+// B_MN: B is stored [K, N] row-major (N contiguous: the weight W itself for
+// dgrad, instead of a transposed copy); its tiles are loaded and described
+// MN-major (UMMA SWIZZLE_128B MN-major canonical layout: 128-byte rows of N,
+// 8-row K groups 1024 B apart), the instruction descriptor's b_major bit set.
+template <bool OUT_BF16, int STAGES, bool TMA_EPI, int EPI_WARPS, int BN, bool B_MN = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32, 1)
     gemm_mxf8_2cta_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
@@ -190,7 +194,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * cta_bytes);
                     const uint32_t fl = full_leader0 + stage * 8;
                     tma_load_2d_2sm(s_a + stage * L::A_BYTES, &tmA, fl, kb * G2_BK, mb * G2_BM);
-                    tma_load_2d_2sm(s_b + stage * L::B_BYTES, &tmB, fl, kb * G2_BK, n0);
+                    if (B_MN)
+                        tma_load_2d_2sm(s_b + stage * L::B_BYTES, &tmB, fl, n0, kb * G2_BK);
+                    else
+                        tma_load_2d_2sm(s_b + stage * L::B_BYTES, &tmB, fl, kb * G2_BK, n0);
                     tma_load_2d_2sm(s_sfa + stage * L::SFA_BYTES, &tmSFA, fl, 0,
                                     sf_row_of_chunk((int64_t)mb * kblocks + kb));
                     if (!unit_b) {
@@ -223,9 +230,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
             }
             int stage = 0;
             uint32_t phase = 0, acc_phase = 0, sfbuf = 0;   // acc_phase bit a: parity of accumulator stage a
-            constexpr uint32_t idesc0 = mxf8_idesc(2 * G2_BM, BN, 0, 0);
+            constexpr uint32_t idesc0 = mxf8_idesc(2 * G2_BM, BN, 0, 0) | (B_MN ? (1u << 16) : 0u);
             const uint64_t adesc0 = umma_desc(smem_u32(s_a), 0, 1024, kLayoutSW128);
-            const uint64_t bdesc0 = umma_desc(smem_u32(s_b), 0, 1024, kLayoutSW128);
+            // MN-major: LBO = stride between 128-element N blocks (one block per CTA
+            // at BN = 256: unused), SBO = 1024 B between 8-row K groups
+            const uint64_t bdesc0 = umma_desc(smem_u32(s_b), B_MN ? L::B_BYTES : 0, 1024, kLayoutSW128);
             const uint64_t sfadesc0 = umma_desc(smem_u32(s_sfa), 0, 128, kLayoutNone);
             const uint64_t sfbdesc0 = umma_desc(smem_u32(s_sfb), 0, 128, kLayoutNone);
             auto copy_sf = [&](uint32_t sa, uint32_t sb) {
@@ -262,7 +271,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                         const uint64_t bdesc = bdesc0 + (uint64_t)((stage * L::B_BYTES) >> 4);
 #pragma unroll
                         for (int k = 0; k < G2_BK / 32; ++k)
-                            mma_mxf8_2cta(tmem + acc * BN, adesc + 2 * k, bdesc + 2 * k,
+                            mma_mxf8_2cta(tmem + acc * BN, adesc + 2 * k, bdesc + (B_MN ? 256 * k : 2 * k),
                                           idesc0 | ((uint32_t)k << 29) | ((uint32_t)k << 4), sa, sb, (kb | k) != 0);
                         tc_commit_2cta_mc(&empty[stage], 0x3);
                     }
@@ -423,12 +432,12 @@ static int g2_raster(int64_t m_pairs, int64_t n_tiles, int BN, int64_t K) {
     return bytes_m <= bytes_n ? (int)gm : -(int)gn;
 }
 
-template <bool OUT_BF16, int STAGES, bool TMA_EPI, int EPI_WARPS, int BN = 256>
+template <bool OUT_BF16, int STAGES, bool TMA_EPI, int EPI_WARPS, int BN = 256, bool B_MN = false>
 static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
                           const float* sB, void* D, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
                           cudaStream_t st) {
     using L = G2Layout<STAGES, TMA_EPI, EPI_WARPS, BN>;
-    auto kern = gemm_mxf8_2cta_kernel<OUT_BF16, STAGES, TMA_EPI, EPI_WARPS, BN>;
+    auto kern = gemm_mxf8_2cta_kernel<OUT_BF16, STAGES, TMA_EPI, EPI_WARPS, BN, B_MN>;
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM) != cudaSuccess)
@@ -439,7 +448,8 @@ static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B
     const int64_t sfa_rows = ((M + 127) / 128) * (K / 128) * 2;
     const int64_t sfb_rows = ((N + 127) / 128) * (K / 128) * 2;
     if (!make_tmap_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, A, M, K, 128, G2_BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, B, N, K, 128, BN / 2, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !(B_MN ? make_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, B, K, N, BN / 2, G2_BK, CU_TENSOR_MAP_SWIZZLE_128B)
+               : make_tmap_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, B, N, K, 128, BN / 2, CU_TENSOR_MAP_SWIZZLE_128B)) ||
         !make_tmap_2d(&tsa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, SFA, sfa_rows, 256, 256, 2, CU_TENSOR_MAP_SWIZZLE_NONE))
         return MOSS_ERR_CUDA;
     tsb = tsa;
@@ -494,6 +504,16 @@ int launch_gemm2(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const u
                   : launch_gemm2_t<false, 8, true, 8, 128>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
     return bf ? launch_gemm2_t<true, 6, true, 8>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
               : launch_gemm2_t<false, 6, true, 8>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
+}
+
+// dgrad with the weight as stored: B = W [K, N] row-major, per-tensor (unit SF)
+int launch_gemm2_bkn(const uint8_t* A, const uint8_t* SFA, const uint8_t* B_kn, const float* sA, const float* sB,
+                     void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, cudaStream_t st) {
+    if (M % (2 * G2_BM) || N % G2_BN || K % G2_BK) return MOSS_ERR_SHAPE;
+    if ((reinterpret_cast<uintptr_t>(D) % 16) || (ldd * (d_dtype == MOSS_BF16 ? 2 : 4)) % 16) return MOSS_ERR_ALIGN;
+    return d_dtype == MOSS_BF16
+               ? launch_gemm2_t<true, 6, true, 8, 256, true>(A, SFA, B_kn, nullptr, sA, sB, D, ldd, M, N, K, 0, st)
+               : launch_gemm2_t<false, 6, true, 8, 256, true>(A, SFA, B_kn, nullptr, sA, sB, D, ldd, M, N, K, 0, st);
 }
 
 }  // namespace moss

@@ -164,6 +164,23 @@ def mx_gemm(a_codes: torch.Tensor, a_sf: torch.Tensor | None, s_a: torch.Tensor,
     return d[:m, :n] if padded else d
 
 
+def mx_gemm_bkn(a_codes: torch.Tensor, a_sf: torch.Tensor, s_a: torch.Tensor, w_codes: torch.Tensor,
+                s_w: torch.Tensor, *, out_dtype: torch.dtype = torch.bfloat16) -> torch.Tensor:
+    """D[M, N] = (A . SFA) W * s_a * s_w with W = w_codes [K, N] as stored (per-tensor
+    E4M3, unit scales): the dgrad product dX = dY W without a transposed copy of W
+    (MN-major tcgen05 B operand).  Shapes off the kernel's grid (M % 256, N % 256,
+    K % 128) go through ``mx_gemm`` with W^T materialised."""
+    m, k = a_codes.shape
+    kw, n = w_codes.shape
+    if k != kw:
+        raise InvalidShapeError(f"K mismatch: {k} vs {kw}")
+    if m % 256 or n % 256 or k % 128 or not w_codes.is_contiguous() or not a_codes.is_contiguous():
+        return mx_gemm(a_codes, a_sf, s_a, w_codes.t().contiguous(), None, s_w, out_dtype=out_dtype)
+    d = torch.empty((m, n), dtype=out_dtype, device=a_codes.device)
+    _lib.gemm_bkn(a_codes, a_sf, w_codes, s_a, s_w, d)
+    return d
+
+
 def gemm_mx_epilogue(ops: GemmOperands) -> tuple[torch.Tensor, GemmCounters]:
     """C = W X^T with all FP32 dequantisation in the epilogue (gemm.py:115-129).
 

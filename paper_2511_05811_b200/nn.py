@@ -35,7 +35,7 @@ from . import _lib
 from .autoscale import ScaleSchedule, auto_scale_advance, rescale_due
 from .errors import InvalidArgumentError, InvalidShapeError
 from .fp8 import E4M3
-from .gemm import mx_gemm
+from .gemm import mx_gemm, mx_gemm_bkn
 from .optim import adam_params
 from .quantize import quantize_mx2
 
@@ -115,7 +115,7 @@ class MossLinearFunction(torch.autograd.Function):
         opd = quantize_mx2(dy2d, row=need_x, col=ctx.need_w, flags=flags, amax=layer.take_dy_amax(dy2d))
         dx = None
         if need_x:
-            dx = mx_gemm(opd.codes, opd.sf, opd.g, layer.w_fp8_t, None, layer.w_scale, out_dtype=torch.bfloat16)
+            dx = mx_gemm_bkn(opd.codes, opd.sf, opd.g, layer.w_fp8, layer.w_scale)   # dY W, W as stored
             dx = dx.view(ctx.x_shape)
             if dx.dtype != ctx.x_dtype:
                 dx = dx.to(ctx.x_dtype)
@@ -183,8 +183,6 @@ class MossLinear(nn.Module):
         self.weight.moss_layer = self
         self.register_buffer("w_fp8", torch.zeros(out_features, in_features, dtype=torch.uint8, device=device),
                              persistent=False)
-        self.register_buffer("w_fp8_t", torch.zeros(in_features, out_features, dtype=torch.uint8, device=device),
-                             persistent=False)
         self.register_buffer("w_scale", torch.ones(1, dtype=torch.float32, device=device), persistent=False)
         self.register_buffer("w_amax", torch.zeros(1, dtype=torch.float32, device=device), persistent=False)
         self.interval = interval
@@ -196,6 +194,12 @@ class MossLinear(nn.Module):
         # set by zero.Zero1 when this weight's FP8 codes arrive by an async
         # all-gather: a callable that makes the current stream wait for them
         self.fp8_pending = None
+
+    @property
+    def w_fp8_t(self) -> torch.Tensor:
+        """W_fp8^T as a view: no transposed copy is kept — the dgrad GEMM reads
+        W_fp8 [out, in] as stored through an MN-major operand (gemm.mx_gemm_bkn)."""
+        return self.w_fp8.t()
 
     def offer_dy_amax(self, dy: torch.Tensor) -> torch.Tensor:
         """Called by the producer of dY before it launches: returns the amax
@@ -226,11 +230,10 @@ class MossLinear(nn.Module):
 
     @torch.no_grad()
     def encode_weight(self) -> None:
-        """W_fp8 = e4m3(f32(W)/f32(s_t)) (train.py:113-118) + transpose, one launch."""
+        """W_fp8 = e4m3(f32(W)/f32(s_t)) (train.py:113-118), one launch."""
         s = float(np.float32(self.schedule.s_t))
         self.w_scale.fill_(s)
-        _lib.encode_scaled(self.weight.detach(), device_flags(self.weight.device), scale_host=s,
-                           codes=self.w_fp8, codes_t=self.w_fp8_t if self.out_features % 32 == 0 else None)
+        _lib.encode_scaled(self.weight.detach(), device_flags(self.weight.device), scale_host=s, codes=self.w_fp8)
 
     def forward(self, x: torch.Tensor, amax: torch.Tensor | None = None) -> torch.Tensor:
         if self.schedule is None:
@@ -403,7 +406,7 @@ class MossAdamW:
                 _lib.adamw_fp8_dev(p.data, g, m, v, rows, cols, p_dev, None, flags, w_amax=layer.w_amax)
             else:
                 _lib.adamw_fp8_dev(p.data, g, m, v, rows, cols, p_dev, p_dev + 36, flags, scale_out=layer.w_scale,
-                                   w_fp8=layer.w_fp8, w_fp8_t=layer.w_fp8_t, w_amax=layer.w_amax,
+                                   w_fp8=layer.w_fp8, w_amax=layer.w_amax,
                                    n_saturated=self.saturations)
         if rescale:
             self._finish_rescale()

@@ -15,11 +15,11 @@ MossLinear weight W (the FP8 linears, ~96 % of a Llama's parameters):
     bytes per parameter instead of 8);
   * the E4M3 codes of every slice are all-gathered (1 byte per parameter on
     the wire, not 4: the FP8 all-gather) into the codes buffer the forward
-    GEMMs read, and each rank rebuilds the dgrad operand W_fp8^T locally with
-    a byte transpose (per-tensor codes commute with the transpose).  With
+    GEMMs read; the dgrad GEMM reads the same codes as an MN-major operand, so
+    no transposed copy has to be rebuilt.  With
     ``overlap_gather`` (default) the all-gathers are issued asynchronously in
     forward layer order at the end of ``step`` and each MossLinear waits for
-    its bucket's gather (and transposes) only when the next forward reaches
+    its bucket's gather only when the next forward reaches
     it, so the exchange overlaps the preceding layers' forward compute;
   * scales: s_t advances on the host identically on every rank
     (autoscale.py:71-79, O(1), no data); a rescale step (autoscale.py:86-96)
@@ -235,7 +235,9 @@ class Zero1:
         layer.w_scale.copy_(self.opt.hp_dev[idx * w + 9: idx * w + 10])
 
     def _transpose(self, layer) -> None:
-        _lib.transpose_u8(layer.w_fp8, layer.w_fp8_t)
+        """Nothing to rebuild: the dgrad GEMM reads W_fp8 as stored (MN-major
+        operand, gemm.mx_gemm_bkn), so the gathered codes are the whole update.
+        (tests/test_zero_cpu.py swaps in a host transpose for its stub layers.)"""
 
     # ------------------------------------------------------------------ step
     @torch.no_grad()
@@ -306,7 +308,7 @@ class Zero1:
         return arrived
 
     def sync(self) -> None:
-        """Complete every pending FP8 all-gather (codes and transposes current)."""
+        """Complete every pending FP8 all-gather (codes current on this rank)."""
         for p in self.moss:
             layer = p.moss_layer
             if layer.fp8_pending is not None:
