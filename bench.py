@@ -362,7 +362,9 @@ def main() -> None:
         opt = MossAdamW(model, lr=3e-4, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1)
         T = args.tokens
         torch.manual_seed(4321 + rank)   # per-rank batch shard
-        x = torch.randn(T, model.d, device=dev, dtype=torch.bfloat16)
+        # the step's input requires grad: all 12 GEMMs (fwd, dgrad, wgrad of the 4 linears) run,
+        # matching the FLOP count (the first layer's dgrad is the gradient a real model passes down)
+        x = torch.randn(T, model.d, device=dev, dtype=torch.bfloat16).requires_grad_(True)
         flops_step = float(model.gemm_flops_per_token()) * T
         fwd = model
     if args.zero1:
@@ -385,6 +387,8 @@ def main() -> None:
             buckets.reset()
         else:
             opt.zero_grad()
+        if xin.is_floating_point():
+            xin = xin.detach().requires_grad_(True)   # fresh leaf: dX of the first layer is computed, not accumulated
         loss = fwd_bwd(xin)
         if hasattr(buckets, "step"):
             buckets.step()
@@ -429,7 +433,7 @@ def main() -> None:
     runner = step
     if use_graph:
         from paper_2511_05811_b200.nn import CudaGraphStep
-        static_x = x.clone()
+        static_x = x.detach().clone().requires_grad_(x.requires_grad)
         graphed = CudaGraphStep(fwd_bwd, opt, (static_x,))
         runner = lambda xin: graphed(xin)
         for _ in range(3):          # first call is eager + capture, then replays

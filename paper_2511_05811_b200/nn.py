@@ -458,7 +458,14 @@ class CudaGraphStep:
 
     def __init__(self, step_fn, opt: MossAdamW, static_inputs: tuple, zero_grad=None):
         self.fn, self.opt, self.inputs = step_fn, opt, static_inputs
-        self.zero_grad = zero_grad or (lambda: opt.zero_grad(set_to_none=True))
+        base = zero_grad or (lambda: opt.zero_grad(set_to_none=True))
+
+        def zero_all():
+            base()
+            for t in self.inputs:                 # inputs that require grad (dX of the first layer)
+                if isinstance(t, torch.Tensor) and t.requires_grad:
+                    t.grad = None
+        self.zero_grad = zero_all
         self.graph = None
         self.loss = None
 
@@ -480,9 +487,10 @@ class CudaGraphStep:
         torch.cuda.current_stream().wait_stream(s)
 
     def __call__(self, *inputs) -> torch.Tensor:
-        for dst, src in zip(self.inputs, inputs):
-            if src is not dst:
-                dst.copy_(src, non_blocking=True)
+        with torch.no_grad():                       # static inputs may be leaves that require grad
+            for dst, src in zip(self.inputs, inputs):
+                if src is not dst:
+                    dst.copy_(src, non_blocking=True)
         if self.opt.rescale_due_next() or self.graph is None:
             # eager step (rescale, or the step before the first capture)
             self.zero_grad()
