@@ -481,7 +481,8 @@ def main() -> None:
                 cstream.wait_event(s2)
                 if i >= 2:
                     cstream.wait_event(consumed[b])          # step i-2 is done reading this buffer
-                stage[b].copy_(x_host, non_blocking=True)
+                with torch.no_grad():
+                    stage[b].copy_(x_host, non_blocking=True)
                 ready[b].record(cstream)
 
         prefetch(0)

@@ -193,8 +193,10 @@ int moss_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q
  * mode 3 scale:  out = x * (*scale)                                    (scale: device f32) */
 int moss_glue(int mode, const void* x, const void* y, const float* scale, void* out, float* amax, int64_t T,
               int64_t d, void* stream);
-/* *acc = sum x^2 (f32) over n bf16 elements (n % 8 == 0) */
-int moss_sumsq(const void* x, int64_t n, float* acc, void* stream);
+/* *acc = sum x^2 (f32) over n bf16 elements (n % 8 == 0); deterministic (fixed-order
+ * reduction through `partials`, MOSS_SUMSQ_PARTIALS floats of caller scratch) */
+#define MOSS_SUMSQ_PARTIALS 1024
+int moss_sumsq(const void* x, int64_t n, float* acc, float* partials, void* stream);
 /* Cross entropy of bf16 logits [T, V] (V % 8 == 0) against int64 targets:
  * fwd  lse[t] = logsumexp(x[t, :]) (f32, one read of the row), loss[t] = lse[t] - x[t, y_t]
  * bwd  dlogits = (softmax(x) - onehot(y)) * (*scale), bf16; scale a device f32 (dL/dmean / T) */

@@ -48,7 +48,7 @@ _SIGS = {
     "moss_cross_entropy_fwd": (_I, [_P, _P, _P, _P, _I64, _I64, _P]),
     "moss_glue": (_I, [_I, _P, _P, _P, _P, _P, _I64, _I64, _P]),
     "moss_gemm_mxf8_bkn": (_I, [_P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _P]),
-    "moss_sumsq": (_I, [_P, _I64, _P, _P]),
+    "moss_sumsq": (_I, [_P, _I64, _P, _P, _P]),
     "moss_cross_entropy_bwd": (_I, [_P, _P, _P, _P, _P, _I64, _I64, _P]),
     "moss_quant_per_group": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P, _P]),
     "moss_gemm_pergroup": (_I, [_P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _P]),
@@ -399,6 +399,11 @@ def glue(mode: int, x, out, amax, *, y=None, scale=None, T: int, d: int) -> None
               "moss_glue")
 
 
+SUMSQ_PARTIALS = 1024       # include/moss_b200.h MOSS_SUMSQ_PARTIALS
+
+
 def sumsq(x, acc) -> None:
+    """acc[0] = sum x^2 (f32, fixed-order: reproducible); acc must hold 1 + SUMSQ_PARTIALS floats
+    (the tail is the kernel's scratch)."""
     with _Span("producer", x.numel() * 2):
-        check(lib().moss_sumsq(x.data_ptr(), x.numel(), acc.data_ptr(), stream()), "moss_sumsq")
+        check(lib().moss_sumsq(x.data_ptr(), x.numel(), acc.data_ptr(), acc.data_ptr() + 4, stream()), "moss_sumsq")

@@ -39,7 +39,7 @@ int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float*
 int launch_transpose_u8(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t st);
 int launch_glue(int mode, const void* x, const void* y, const float* scale, void* out, float* amax, int64_t T,
                 int64_t d, cudaStream_t st);
-int launch_sumsq(const void* x, int64_t n, float* acc, cudaStream_t st);
+int launch_sumsq(const void* x, int64_t n, float* acc, float* parts, cudaStream_t st);
 int launch_xent_fwd(const void* logits, const int64_t* targets, float* lse, float* loss, int64_t T, int64_t V,
                     cudaStream_t st);
 int launch_xent_bwd(const void* logits, const int64_t* targets, const float* lse, const float* scale, void* dlogits,
@@ -250,11 +250,11 @@ int moss_glue(int mode, const void* x, const void* y, const float* scale, void* 
     return moss::launch_glue(mode, x, y, scale, out, amax, T, d, (cudaStream_t)stream);
 }
 
-int moss_sumsq(const void* x, int64_t n, float* acc, void* stream) {
+int moss_sumsq(const void* x, int64_t n, float* acc, float* partials, void* stream) {
     if (n <= 0 || n % 8) return MOSS_ERR_SHAPE;
-    if (!x || !acc) return MOSS_ERR_ARGUMENT;
+    if (!x || !acc || !partials) return MOSS_ERR_ARGUMENT;
     if (!al16(x)) return MOSS_ERR_ALIGN;
-    return moss::launch_sumsq(x, n, acc, (cudaStream_t)stream);
+    return moss::launch_sumsq(x, n, acc, partials, (cudaStream_t)stream);
 }
 
 int moss_cross_entropy_fwd(const void* logits, const int64_t* targets, float* lse, float* loss, int64_t T, int64_t V,

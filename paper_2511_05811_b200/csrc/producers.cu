@@ -509,9 +509,12 @@ __global__ void __launch_bounds__(256) glue_kernel(const __nv_bfloat16* __restri
     block_amax_commit(m, red_u, amax);
 }
 
-// sum of squares of a bf16 tensor in f32 -> *acc (atomicAdd per CTA; zeroed by the launcher)
+// sum of squares of a bf16 tensor in f32, deterministic: per-CTA partials in a
+// fixed-size buffer, then one CTA reduces them in a fixed order (no atomics:
+// the loss is bit-reproducible across runs and CUDA-graph replays)
+constexpr int SUMSQ_PARTS = 1024;
 __global__ void __launch_bounds__(256) sumsq_kernel(const __nv_bfloat16* __restrict__ x, int64_t nvec,
-                                                    float* __restrict__ acc) {
+                                                    float* __restrict__ parts) {
     __shared__ float red[8];
     float ssum = 0.f;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
@@ -521,7 +524,15 @@ __global__ void __launch_bounds__(256) sumsq_kernel(const __nv_bfloat16* __restr
         for (int k = 0; k < 8; ++k) ssum = fmaf(v[k], v[k], ssum);
     }
     ssum = block_sum<256>(ssum, red);
-    if (threadIdx.x == 0) atomicAdd(acc, ssum);
+    if (threadIdx.x == 0) parts[blockIdx.x] = ssum;
+}
+
+__global__ void __launch_bounds__(SUMSQ_PARTS) sumsq_final_kernel(const float* __restrict__ parts, int n,
+                                                                  float* __restrict__ acc) {
+    __shared__ float red[SUMSQ_PARTS / 32];
+    float v = threadIdx.x < n ? parts[threadIdx.x] : 0.f;
+    v = block_sum<SUMSQ_PARTS>(v, red);
+    if (threadIdx.x == 0) *acc = v;
 }
 
 // ------------------------------------------------------------------ cross entropy (LM head)
@@ -735,11 +746,11 @@ int launch_glue(int mode, const void* x, const void* y, const float* scale, void
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 
-int launch_sumsq(const void* x, int64_t n, float* acc, cudaStream_t st) {
-    if (cudaMemsetAsync(acc, 0, 4, st) != cudaSuccess) return MOSS_ERR_CUDA;
+int launch_sumsq(const void* x, int64_t n, float* acc, float* parts, cudaStream_t st) {
     const int64_t nvec = n / 8;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nvec + 255) / 256, (int64_t)sm_count() * 8));
-    sumsq_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, nvec, acc);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nvec + 255) / 256, SUMSQ_PARTS));
+    sumsq_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, nvec, parts);
+    sumsq_final_kernel<<<1, SUMSQ_PARTS, 0, st>>>(parts, grid, acc);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 

@@ -482,7 +482,10 @@ class CudaGraphStep:
         self.graph = torch.cuda.CUDAGraph()
         self.zero_grad()
         with torch.cuda.graph(self.graph, stream=s):
-            self.loss = self.fn(*self.inputs)
+            # detached: the captured autograd graph (and the AccumulateGrad nodes bound to
+            # this capture stream) must not outlive the capture, or a later capture of
+            # the same model on another stream picks up a cross-stream dependency
+            self.loss = self.fn(*self.inputs).detach()
             self.opt.launch(False)
         torch.cuda.current_stream().wait_stream(s)
 

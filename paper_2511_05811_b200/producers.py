@@ -223,11 +223,11 @@ class MeanSquareFn(torch.autograd.Function):
     def forward(ctx, y, consumer):
         d = y.shape[-1]
         y2 = _c2(y, d)
-        acc = torch.empty(1, dtype=torch.float32, device=y.device)
+        acc = torch.empty(1 + _lib.SUMSQ_PARTIALS, dtype=torch.float32, device=y.device)
         _lib.sumsq(y2, acc)
         ctx.save_for_backward(y2)
         ctx.consumer, ctx.shape = consumer, y.shape
-        return (acc / y2.numel()).reshape(())
+        return (acc[:1] / y2.numel()).reshape(())
 
     @staticmethod
     def backward(ctx, g):

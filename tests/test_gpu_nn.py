@@ -116,3 +116,34 @@ def test_layer_stack_trains():
         losses.append(float(loss))
     opt.check()
     assert losses[-1] < 0.5 * losses[0]
+
+
+def test_two_graph_steps_same_model_double_buffered():
+    """Two CudaGraphSteps over one model/optimizer (double-buffered inputs, as the
+    e2e pipeline uses them): both capture, and alternating replays give the same
+    losses as a single graph fed by copies."""
+    from paper_2511_05811_b200.nn import CudaGraphStep, MossAdamW
+    from paper_2511_05811_b200.workloads import LayerStack
+
+    def run(two):
+        torch.manual_seed(0)
+        model = LayerStack(d_model=512, d_ffn=1024, device="cuda")
+        opt = MossAdamW(model, lr=1e-3)
+
+        def fb(xin):
+            loss = model(xin)
+            loss.backward()
+            return loss
+        g = torch.Generator(device="cuda").manual_seed(5)
+        data = [torch.randn(512, 512, device="cuda", dtype=torch.bfloat16, generator=g) for _ in range(8)]
+        bufs = [torch.zeros(512, 512, device="cuda", dtype=torch.bfloat16).requires_grad_(True) for _ in range(2)]
+        steps = [CudaGraphStep(fb, opt, (bufs[b],)) for b in range(2 if two else 1)]
+        out = []
+        for i, x in enumerate(data):
+            b = i % len(steps)
+            with torch.no_grad():
+                bufs[b].copy_(x)
+            out.append(float(steps[b](bufs[b])))
+        return out
+
+    assert run(True) == run(False)
