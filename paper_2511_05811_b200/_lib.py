@@ -405,5 +405,5 @@ SUMSQ_PARTIALS = 1024       # include/moss_b200.h MOSS_SUMSQ_PARTIALS
 def sumsq(x, acc) -> None:
     """acc[0] = sum x^2 (f32, fixed-order: reproducible); acc must hold 1 + SUMSQ_PARTIALS floats
     (the tail is the kernel's scratch)."""
-    with _Span("producer", x.numel() * 2):
+    with _Span("producer", x.numel() * 2, kernels=2):
         check(lib().moss_sumsq(x.data_ptr(), x.numel(), acc.data_ptr(), acc.data_ptr() + 4, stream()), "moss_sumsq")
