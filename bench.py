@@ -18,8 +18,17 @@ e2e: the same step with the input copied from pinned host memory and the loss
 roofline: the dominant kernel (the GEMM), FLOPs per launch / CUDA-event
   duration per launch over the timed region, vs 2x the measured dense bf16
   peak (MEASURED_PEAKS.json; fp8 dense = 2x bf16 on B200).
+  The peak is cuBLASLt MXFP8 (8192^3) measured in the same run, sustained
+  (back-to-back for ~3 s, the kernel is timed inside a long step) and burst.
 cpu_baseline / --impl reference: the CPU oracle port (oracle/numpy_ref, the
-  reference's own numpy dataflow) timed on a bounded sample on the host cores.
+  reference's own numpy dataflow) timed on ONE bounded sample of the same
+  workload (REF_SAMPLE below), on the host cores; the reference arm prints
+  exactly this arm's ``config``.
+--gpus N (N > 1) without WORLD_SIZE in the environment re-executes itself
+  under torchrun with N ranks (one per GPU, NCCL); under torchrun the world
+  size must equal --gpus.  Every N runs the same timing mode (CUDA-graph
+  replays, the NCCL collectives captured in the graph) and reports the
+  Llama-2-7B-shape step (configs[3]/[4]) tokens/s beside the layer value.
 """
 
 from __future__ import annotations
@@ -60,7 +69,46 @@ def parse():
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
     ap.add_argument("--zero1", action="store_true",
                     help="N>1: ZeRO-1 (reduce-scatter grads, sharded K3, FP8 all-gather) instead of all-reduce DP")
+    ap.add_argument("--no-fp8-roof", action="store_true", help="skip the cuBLASLt MXFP8 roof measurement")
+    ap.add_argument("--llama-steps", type=int, default=8, help="default line: timed steps of the 7B sub-measure")
+    ap.add_argument("--launch-probe", action="store_true",
+                    help="test hook: spawn/check the ranks, print who ran, touch no GPU")
     return ap.parse_args()
+
+
+_BLAS_LIMITS = None
+
+
+def free_port() -> int:
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def maybe_spawn(args) -> int | None:
+    """--gpus N > 1 outside torchrun: run this script under torchrun with N
+    ranks (the driver's own launch line) and return its exit code."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def launch_probe(args, world: int, rank: int, local: int) -> None:
+    import torch.distributed as dist
+    info = {"rank": rank, "local_rank": local, "pid": os.getpid(), "world": world}
+    infos = [info]
+    if world > 1:
+        dist.init_process_group("gloo", init_method="env://")
+        infos = [None] * world
+        dist.all_gather_object(infos, info)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"launch_probe": True, "n_gpus": world, "gpus_flag": args.gpus, "ranks": infos}), flush=True)
 
 
 # ------------------------------------------------------------------ CPU oracle leg
@@ -112,40 +160,66 @@ def cpu_linear_step(tokens: int, d_in: int, d_out: int, seed: int = 0, ops: dict
     return time.perf_counter() - t0
 
 
+# The ONE bounded CPU sample of the workload, shared by cpu_baseline (our arm)
+# and the reference arm: a quarter of configs[0] (BASELINE configs[0] is
+# tokens = K = N = 4096; its full size is ~36 s per step through the port,
+# ~15 min for the driver's 25 steps).  tools/ref_vs_port_timing.py times the
+# literal mossq against the port on this sample (profiles/r02_ref_vs_port.txt).
+REF_SAMPLE = {"tokens": 1024, "d": 4096}
+
+
+def ref_sample_desc() -> str:
+    return (f"one MOSS linear fwd+dgrad+wgrad+AdamW/autoscale step, tokens={REF_SAMPLE['tokens']}, "
+            f"{REF_SAMPLE['d']}x{REF_SAMPLE['d']} (1/4 of configs[0]), oracle/numpy_ref (the reference's numpy "
+            f"dataflow: per-32-block float64 GEMMs, float64 AdamW), all host threads")
+
+
 def cpu_sample(tokens: int, d: int, reps: int = 1) -> dict:
     ops: dict = {}
     secs = min(cpu_linear_step(tokens, d, d, seed=r, ops=ops) for r in range(reps))
     flops = 6.0 * tokens * d * d
     return {"value": flops / secs / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"one MOSS linear fwd+dgrad+wgrad+AdamW step, tokens={tokens}, {d}x{d}, oracle/numpy_ref "
-                      f"(reference numpy dataflow, float64 block GEMMs), {secs:.2f} s",
+            "sample": ref_sample_desc() + f"; {secs:.2f} s",
             "per_op_seconds": {k: round(v / reps, 4) for k, v in ops.items()},
             "seconds": secs}
 
 
-def run_reference(args, rank: int) -> None:
+def run_reference(args, world: int, rank: int) -> None:
+    """Reference arm: the reference's CPU path (the oracle port) on REF_SAMPLE
+    per step, rank 0 only; same metric/unit/config as this script's GPU arm."""
     if rank != 0:
         return
-    tokens, d = 256, 2048
-    for _ in range(args.warmup):
-        cpu_linear_step(tokens, d, d)
+    tokens, d = REF_SAMPLE["tokens"], REF_SAMPLE["d"]
+    for i in range(args.warmup):
+        cpu_linear_step(tokens, d, d, seed=1000 + i)
     t0 = time.perf_counter()
     for i in range(args.steps):
         cpu_linear_step(tokens, d, d, seed=i)
     secs = (time.perf_counter() - t0) / args.steps
     value = 6.0 * tokens * d * d / secs / 1e12
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64 (reference numpy)", "data": "synthetic",
-            "config": {"workload": LAYER_WORKLOAD,
-                       "sample": f"bounded sample of that workload per step: one MOSS linear fwd+dgrad+wgrad+AdamW, "
-                                 f"tokens={tokens}, {d}x{d}, through the oracle port (reference numpy dataflow)",
-                       "tokens": tokens, "shape": [d, d]},
+            "config": layer_config(args, world),
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
-                             "sample": f"per step: one MOSS linear fwd+dgrad+wgrad+AdamW, tokens={tokens}, "
-                                       f"{d}x{d}, oracle/numpy_ref"},
+                             "sample": "per step: " + ref_sample_desc()},
             "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def layer_config(args, world: int) -> dict:
+    """``config`` of the default line (configs[1] as a training step), shared by both arms."""
+    from paper_2511_05811_b200.workloads import LLAMA7B_SHAPES
+    T = args.tokens
+    par = f"dp{world}"
+    if world > 1:
+        par += (" (ZeRO-1: NCCL reduce-scatter fp32 grads, sharded K3, FP8 all-gather)" if args.zero1
+                else " (NCCL bucketed fp32 grad all-reduce, captured in the step graph)")
+    elif args.zero1:
+        par += " (ZeRO-1 driver)"
+    return {"workload": LAYER_WORKLOAD, "tokens_per_gpu": T, "global_batch_tokens": T * world, "parallelism": par,
+            "gemm_flops_per_step_per_gpu": 6.0 * T * sum(k * n for k, n in LLAMA7B_SHAPES.values()),
+            "l2": "not flushed: per-step working set ~3 GB >> 126 MB L2"}
 
 
 # ------------------------------------------------------------------ library reference for the GEMM roofline
@@ -244,22 +318,53 @@ def quantizer_rates(dev, tokens: int, hbm: float) -> dict:
     return res
 
 
-def llama7b_submeasure() -> dict:
-    """The metric's third component (7B-shape train tokens/s, configs[3]):
-    the full Llama-2-7B-shape decoder step (32 layers, seq 4096, batch 1,
-    MOSS FP8 linears, CUDA-graph replays), measured in a child process so its
-    ~160 GB do not share the allocator with the layer workload."""
-    cmd = [sys.executable, os.path.abspath(__file__), "--workload", "llama7b", "--steps", "6", "--warmup", "3",
-           "--no-cpu-baseline", "--no-e2e"]
-    try:
-        out = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
-        d = json.loads(out.stdout.strip().splitlines()[-1])
-        return {"tokens_per_s": d["value"], "ms_per_step": d["ms_per_step"], "steps": d["steps"],
-                "config": d["config"]["workload"], "gemm_tflops_in_step": d["roofline"]["achieved"],
-                "gemm_share_of_step": d["roofline"]["share_of_step"], "clocks": d["clocks"],
-                "peak_allocated_gb": d.get("memory", {}).get("peak_allocated_gb")}
-    except Exception as ex:  # noqa: BLE001 - a sub-measurement must not sink the bench line
-        return {"error": str(ex)[:200]}
+def fp8_roof(dev, gpu_index: int, seconds: float = 3.0) -> dict:
+    """The FP8 roofline denominator, measured: cuBLASLt MXFP8 (torch
+    F.scaled_mm, BlockWise1x32 E8M0 scales, bf16 out) at 8192^3.  burst = best
+    single launch of 10 (a kernel timed alone); sustained = back-to-back
+    launches for ``seconds`` under the power cap (a kernel timed inside a long
+    step), with the SM clocks of each.  A library measurement, not the product."""
+    import torch
+    import torch.nn.functional as F
+
+    from paper_2511_05811_b200.quantize import quantize_mx2
+    n = 8192
+    a = torch.randn(n, n, device=dev, dtype=torch.bfloat16)
+    b = torch.randn(n, n, device=dev, dtype=torch.bfloat16)
+    qa, qb = quantize_mx2(a), quantize_mx2(b)
+    A8, B8 = qa.codes.view(torch.float8_e4m3fn), qb.codes.view(torch.float8_e4m3fn).t()
+    sa, sb = qa.sf.view(torch.float8_e8m0fnu), qb.sf.view(torch.float8_e8m0fnu)
+
+    def cub():
+        return F.scaled_mm(A8, B8, sa, F.ScalingType.BlockWise1x32, sb, F.ScalingType.BlockWise1x32,
+                           swizzle_a=F.SwizzleType.SWIZZLE_32_4_4, swizzle_b=F.SwizzleType.SWIZZLE_32_4_4,
+                           output_dtype=torch.bfloat16)
+    flops = 2.0 * n ** 3
+    for _ in range(5):
+        cub()
+    torch.cuda.synchronize()
+    best = float("inf")
+    with ClockSampler(gpu_index) as ck_b:
+        for _ in range(10):
+            s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            cub()
+            e0.record()
+            torch.cuda.synchronize()
+            best = min(best, s0.elapsed_time(e0))
+    reps = max(20, int(seconds * 1e3 / best))
+    with ClockSampler(gpu_index) as ck_s:
+        s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(reps):
+            cub()
+        e0.record()
+        torch.cuda.synchronize()
+    sus = s0.elapsed_time(e0) / reps
+    return {"burst_tflops": flops / (best / 1e3) / 1e12, "sustained_tflops": flops / (sus / 1e3) / 1e12,
+            "clocks_burst": ck_b.summary(), "clocks_sustained": ck_s.summary(), "sustained_launches": reps,
+            "how": "cuBLASLt MXFP8 via torch F.scaled_mm (BlockWise1x32, SWIZZLE_32_4_4), 8192^3, bf16 out; burst = "
+                   "best of 10 single launches, sustained = %d back-to-back launches (~%.0f s)" % (reps, seconds)}
 
 
 # ------------------------------------------------------------------ clocks
@@ -314,45 +419,56 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ GPU arm
-def main() -> None:
-    args = parse()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+def _max_over_ranks(v: float, dev, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def foreign_launches(step, x) -> dict | None:
+    """Kernels of one eager step that are not ours (torch.profiler / CUPTI):
+    name -> count.  Evidence for ``gpu_launches`` (which counts our kernels)."""
+    import torch
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step(x)
+            torch.cuda.synchronize()
+        out: dict = {}
+        for ev in prof.events():
+            if ev.device_type == torch.autograd.DeviceType.CUDA and "moss::" not in ev.name \
+                    and not ev.name.startswith(("Memcpy", "Memset", "ncclDevKernel")):
+                out[ev.name[:80]] = out.get(ev.name[:80], 0) + 1
+        return out
+    except Exception as ex:  # noqa: BLE001 - evidence only
+        return {"error": str(ex)[:160]}
+
+
+def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: bool) -> dict:
+    """Build one workload, warm it up, time it; returns the measurements.
+    kind: "layer" (configs[1] as a training step) or "llama7b" (configs[3]/[4])."""
     import torch
     import torch.distributed as dist
 
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    elif args.zero1 and args.impl != "reference":
-        import socket
-        sk = socket.socket()
-        sk.bind(("127.0.0.1", 0))
-        port = sk.getsockname()[1]
-        sk.close()
-        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
-    if args.impl == "reference":
-        run_reference(args, rank)
-        if world > 1:
-            dist.destroy_process_group()
-        return
-
     from paper_2511_05811_b200 import _lib
     from paper_2511_05811_b200.dist import GradBuckets
-    from paper_2511_05811_b200.nn import MossAdamW
+    from paper_2511_05811_b200.nn import CudaGraphStep, MossAdamW
     from paper_2511_05811_b200.workloads import LayerStack
 
-    dev = torch.device("cuda", local)
     torch.manual_seed(1234)          # identical initial weights on every rank (DP)
-    if args.workload == "llama7b":
+    if kind == "llama7b":
         from paper_2511_05811_b200.llama import LLAMA2_7B, LlamaConfig, LlamaModel
         from paper_2511_05811_b200.trainer import make_optimizer
         cfg = LlamaConfig(**{**LLAMA2_7B.__dict__, "n_layers": args.layers, "max_seq": args.seq})
         model = LlamaModel(cfg, device=dev)
         opt = make_optimizer(model, 3e-4, 10_000, 100)
         T = args.seq
-        g = torch.Generator(device=dev).manual_seed(99 + rank)
+        g = torch.Generator(device=dev).manual_seed(99 + rank)      # per-rank batch shard
         tok = torch.randint(0, cfg.vocab, (1, T + 1), device=dev, generator=g)
         x, y_tok = tok[:, :-1].contiguous(), tok[:, 1:].contiguous()
         flops_step = float(cfg.gemm_flops_per_token()) * T
@@ -378,8 +494,6 @@ def main() -> None:
     def fwd_bwd(xin):
         loss = fwd(xin)
         loss.backward()
-        if buckets is not None:
-            buckets.finish()
         return loss
 
     def step(xin):
@@ -390,6 +504,8 @@ def main() -> None:
         if xin.is_floating_point():
             xin = xin.detach().requires_grad_(True)   # fresh leaf: dX of the first layer is computed, not accumulated
         loss = fwd_bwd(xin)
+        if buckets is not None:
+            buckets.finish()
         if hasattr(buckets, "step"):
             buckets.step()
         else:
@@ -401,7 +517,6 @@ def main() -> None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    use_graph = world == 1 and not args.no_graph and not args.zero1
     for _ in range(max(3, args.warmup)):
         step(x)
     opt.check("warmup")
@@ -418,7 +533,7 @@ def main() -> None:
     _lib.INSTR.start(timing=True)
     if hasattr(buckets, "timing"):
         buckets.timing = True
-    for _ in range(args.steps):
+    for _ in range(steps):
         torch.cuda._sleep(sleep_cycles)
         step(x)
         torch.cuda.synchronize()
@@ -427,35 +542,37 @@ def main() -> None:
     if hasattr(buckets, "timing"):
         buckets.timing = False
     kern = _lib.INSTR.summary()
-    launches = _lib.INSTR.launches // args.steps
+    launches = _lib.INSTR.launches // steps
+    foreign = foreign_launches(step, x) if rank == 0 else None
     barrier()
 
-    runner = step
-    if use_graph:
-        from paper_2511_05811_b200.nn import CudaGraphStep
-        static_x = x.detach().clone().requires_grad_(x.requires_grad)
-        graphed = CudaGraphStep(fwd_bwd, opt, (static_x,))
-        runner = lambda xin: graphed(xin)
-        for _ in range(3):          # first call is eager + capture, then replays
-            runner(x)
+    # ---- the same timing mode at every N: CUDA-graph replays of the whole step
+    # (forward, backward, the captured NCCL collectives, the optimizer kernels)
+    runner, mode = step, "eager steps"
+    if not args.no_graph:
+        try:
+            static_x = x.detach().clone().requires_grad_(x.requires_grad)
+            graphed = CudaGraphStep(fwd_bwd, opt, (static_x,), buckets=buckets)
+            runner = lambda xin: graphed(xin)
+            for _ in range(3):          # first call is eager + capture, then replays
+                runner(x)
+            mode = "CUDA-graph replays"
+        except Exception as ex:  # noqa: BLE001 - record and time eagerly rather than lose the line
+            runner, mode = step, f"eager steps (graph capture failed: {str(ex)[:120]})"
         barrier()
 
-    # ---- timed region: inputs resident in HBM; working set per step (~3 GB) >> L2
+    # ---- timed region: inputs resident in HBM; working set per step >> L2
     s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev.index) as clocks:
         s_ev.record()
         h0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(steps):
             loss = runner(x)
-        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
+        host_ms = (time.perf_counter() - h0) * 1e3 / steps
         e_ev.record()
         torch.cuda.synchronize()
     barrier()
-    ms = s_ev.elapsed_time(e_ev) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = _max_over_ranks(s_ev.elapsed_time(e_ev) / steps, dev, world)
     opt.check("timed region")
 
     # ---- e2e: input from pinned host memory, loss read back every step.
@@ -464,9 +581,9 @@ def main() -> None:
     # step i's compute; each step's loss is copied D2H into a pinned slot
     # without stalling the host.  All copies are inside the timed region.
     e2e = None
-    if not args.no_e2e:
-        x_host = x.cpu().pin_memory()
-        loss_host = torch.empty(args.steps, dtype=torch.float32).pin_memory()
+    if want_e2e:
+        x_host = x.detach().cpu().pin_memory()
+        loss_host = torch.empty(steps, dtype=torch.float32).pin_memory()
         stage = [torch.empty_like(x) for _ in range(2)]
         cstream = torch.cuda.Stream(device=dev)
         ready = [torch.cuda.Event() for _ in range(2)]
@@ -486,9 +603,9 @@ def main() -> None:
                 ready[b].record(cstream)
 
         prefetch(0)
-        for i in range(args.steps):
+        for i in range(steps):
             b = i % 2
-            if i + 1 < args.steps:
+            if i + 1 < steps:
                 prefetch(i + 1)
             torch.cuda.current_stream().wait_event(ready[b])
             loss = runner(stage[b])
@@ -497,32 +614,144 @@ def main() -> None:
         e2.record()
         torch.cuda.synchronize()
         assert bool(torch.isfinite(loss_host).all()), "non-finite loss in the e2e run"
-        ms_e2e = s2.elapsed_time(e2) / args.steps
-        if world > 1:
-            t = torch.tensor([ms_e2e], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_e2e = float(t.item())
-        e2e = {"value": world * flops_step / (ms_e2e / 1e3) / 1e12, "unit": "TFLOP/s",
-               "h2d_bytes_per_step": x_host.numel() * x_host.element_size(), "d2h_bytes_per_step": 4,
-               "ms_per_step": ms_e2e,
+        ms_e2e = _max_over_ranks(s2.elapsed_time(e2) / steps, dev, world)
+        e2e = {"ms_per_step": ms_e2e, "h2d_bytes_per_step": x_host.numel() * x_host.element_size(),
+               "d2h_bytes_per_step": 4,
                "pipeline": "pinned H2D of step i+1 on a copy stream overlapped with step i; per-step loss D2H async"}
-
     # peak device memory of the training run (weights, optimizer state, FP8 copies,
     # the stashed FP8 activation codes, graph pool), before any side measurement
     peak_gb = torch.cuda.max_memory_allocated(dev) / 1e9
-    if rank != 0:
-        dist.destroy_process_group() if world > 1 else None
-        return
+    return {"ms": ms, "host_ms": host_ms, "kern": kern, "launches": launches, "foreign": foreign, "comm": comm,
+            "clocks": clocks.summary(), "e2e": e2e, "peak_gb": peak_gb, "mode": mode, "flops_step": flops_step,
+            "T": T, "steps": steps}
 
+
+def _free_cuda() -> None:
+    import gc
+
+    import torch
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    torch.cuda.reset_peak_memory_stats()
+
+
+def _rates(kern: dict, steps: int, hbm: float):
+    def rate(kind):
+        d = kern.get(kind)
+        if not d or not d["launches"]:
+            return None
+        return {"launches_per_step": d["launches"] // steps, "ms_per_step": d["ms"] / steps,
+                "achieved_gbs": d["work"] / (d["ms"] / 1e3) / 1e9,
+                "frac_of_hbm": d["work"] / (d["ms"] / 1e3) / 1e9 / hbm}
+    return rate
+
+
+def llama_summary(r: dict, world: int, args) -> dict:
+    g = r["kern"].get("gemm", {"launches": 0, "ms": 1e-9, "work": 0})
+    return {"tokens_per_s": world * r["T"] / (r["ms"] / 1e3), "ms_per_step": r["ms"], "steps": r["steps"],
+            "n_gpus": world, "tokens_per_gpu_per_step": r["T"],
+            "config": (f"configs[3]/[4]: Llama-2-7B-shape decoder training step (d 4096, ffn 11008, 32 heads, vocab "
+                       f"32000, {args.layers} layers, seq {args.seq}, batch 1/GPU), MOSS FP8 linears, bf16 SDPA/norm/"
+                       f"head, MossAdamW over all params; dp{world}" +
+                       (" ZeRO-1" if args.zero1 else (" bucketed NCCL all-reduce" if world > 1 else ""))),
+            "timing_mode": r["mode"],
+            "gemm_tflops_in_step": g["work"] / (g["ms"] / 1e3) / 1e12 if g["launches"] else None,
+            "gemm_share_of_step": (g["ms"] / r["steps"]) / r["ms"] if g["launches"] else None,
+            "collectives": r["comm"], "clocks": r["clocks"], "peak_allocated_gb": r["peak_gb"]}
+
+
+def main() -> None:
+    args = parse()
+    rc = maybe_spawn(args)
+    if rc is not None:
+        sys.exit(rc)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(json.dumps({"error": f"world size {world} != --gpus {args.gpus}"}), flush=True)
+        sys.exit(2)
+    if args.launch_probe:
+        launch_probe(args, world, rank, local)
+        return
+    if args.impl == "reference":
+        # all host threads (torchrun sets OMP_NUM_THREADS=1 per rank; rank 0 is the only worker)
+        for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[k] = str(os.cpu_count())
+        try:
+            from threadpoolctl import threadpool_limits
+            global _BLAS_LIMITS
+            _BLAS_LIMITS = threadpool_limits(os.cpu_count())
+        except Exception:  # noqa: BLE001
+            pass
+        run_reference(args, world, rank)       # CPU only: no process group, no GPU
+        return
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    elif args.zero1:
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{free_port()}", rank=0, world_size=1)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    llama_only = args.workload == "llama7b"
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    bf16_sus = peaks.get("bf16_tflops_sustained", 1400.0)
-    bf16_burst = peaks.get("bf16_tflops", 1590.0)
     hbm = peaks.get("hbm_gbs", 6650.0)
-    fp8_peak = 2.0 * bf16_sus
+
+    main_kind = "llama7b" if llama_only else "layer"
+    r = measure(main_kind, args, dev, rank, world, args.steps, want_e2e=not args.no_e2e)
+    _free_cuda()
+    barrier()
+    llama = None
+    if not llama_only and not args.no_llama:
+        try:
+            rl = measure("llama7b", args, dev, rank, world, args.llama_steps, want_e2e=False)
+            llama = llama_summary(rl, world, args)
+        except Exception as ex:  # noqa: BLE001 - a sub-measurement must not sink the bench line
+            llama = {"error": str(ex)[:300]}
+        _free_cuda()
+        barrier()
+
+    # communicator evidence: which GPUs the ranks drove
+    comm_info = None
+    if world > 1 or args.zero1:
+        me = {"rank": rank, "uuid": str(getattr(torch.cuda.get_device_properties(dev), "uuid", "")),
+              "pci_bus_id": getattr(torch.cuda.get_device_properties(dev), "pci_bus_id", None)}
+        every = [None] * dist.get_world_size()
+        dist.all_gather_object(every, me)
+        comm_info = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                     "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                     "ranks": every, "distinct_devices": len({e["uuid"] for e in every})}
+
+    if rank != 0:
+        barrier()
+        if dist.is_initialized():
+            dist.destroy_process_group()
+        return
+
+    roof = None
+    if not args.no_fp8_roof:
+        try:
+            roof = fp8_roof(dev, local)
+        except Exception as ex:  # noqa: BLE001
+            roof = {"error": str(ex)[:200]}
+    have_roof = roof is not None and "sustained_tflops" in roof
+    fp8_peak = roof["sustained_tflops"] if have_roof else 2.0 * peaks.get("bf16_tflops_sustained", 1400.0)
+    peak_src = ("cuBLASLt MXFP8 8192^3 sustained, measured in this run (fp8 roof; the GEMM is timed inside the step)"
+                if have_roof else "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (no fp8 roof measured)")
+    kern, ms, steps = r["kern"], r["ms"], r["steps"]
     g = kern.get("gemm", {"launches": 0, "ms": 1e-9, "work": 0})
     gemm_tflops = g["work"] / (g["ms"] / 1e3) / 1e12 if g["launches"] else 0.0
     traffic = None
@@ -531,31 +760,27 @@ def main() -> None:
         traffic = prof.get("dram_bytes_per_launch")
     except Exception:
         pass
-
-    def rate(kind):
-        d = kern.get(kind)
-        if not d or not d["launches"]:
-            return None
-        return {"launches_per_step": d["launches"] // args.steps, "ms_per_step": d["ms"] / args.steps,
-                "achieved_gbs": d["work"] / (d["ms"] / 1e3) / 1e9,
-                "frac_of_hbm": d["work"] / (d["ms"] / 1e3) / 1e9 / hbm}
-
-    total_kernel_ms = sum(d["ms"] for d in kern.values()) / args.steps
-    llama = args.workload == "llama7b"
-    if llama:
-        wl = (f"configs[3]/[4]: Llama-2-7B-shape decoder training step (d 4096, ffn 11008, 32 heads, vocab 32000, "
-              f"{args.layers} layers, seq {T}, batch 1/GPU), MOSS FP8 linears, bf16 SDPA/norm/head, "
-              f"MossAdamW over all params")
-        if e2e is not None:
-            e2e = {**e2e, "value": world * T / (e2e["ms_per_step"] / 1e3), "unit": "tokens/s"}
+    rate = _rates(kern, steps, hbm)
+    total_kernel_ms = sum(d["ms"] for d in kern.values()) / steps
+    T, flops_step = r["T"], r["flops_step"]
+    e2e = None
+    if r["e2e"] is not None:
+        me2e = r["e2e"]["ms_per_step"]
+        e2e = {**r["e2e"], "value": (world * T / (me2e / 1e3)) if llama_only
+               else world * flops_step / (me2e / 1e3) / 1e12,
+               "unit": "tokens/s" if llama_only else "TFLOP/s"}
+    if llama_only:
+        wl = llama_summary(r, world, args)["config"]
+        config = {"workload": wl, "tokens_per_gpu": T, "global_batch_tokens": T * world,
+                  "parallelism": f"dp{world}", "l2": "not flushed: per-step working set >> 126 MB L2"}
     else:
-        wl = LAYER_WORKLOAD
+        config = layer_config(args, world)
     line = {
         "metric": METRIC,
-        "value": (world * T / (ms / 1e3)) if llama else world * flops_step / (ms / 1e3) / 1e12,
-        "unit": "tokens/s" if llama else "TFLOP/s",
+        "value": (world * T / (ms / 1e3)) if llama_only else world * flops_step / (ms / 1e3) / 1e12,
+        "unit": "tokens/s" if llama_only else "TFLOP/s",
         "n_gpus": world,
-        "steps": args.steps,
+        "steps": steps,
         "warmup": max(3, args.warmup),
         "ms_per_step": ms,
         "higher_is_better": True,
@@ -563,37 +788,38 @@ def main() -> None:
         "vs_baseline": None,
         "dtype": "e4m3 x e4m3 -> fp32 accumulate (MXFP8, E8M0 block scales); bf16 activations; fp32 master/optimizer",
         "data": "synthetic (randn bf16 activations, N(0,0.02^2) weights, random init)",
-        "config": {"workload": wl, "tokens_per_gpu": T, "global_batch_tokens": T * world,
-                   "parallelism": f"dp{world}" + ((" (ZeRO-1: NCCL reduce-scatter fp32 grads, sharded K3, FP8 all-gather)"
-                                                   if args.zero1 else " (NCCL bucketed fp32 grad all-reduce)")
-                                                  if world > 1 else (" (ZeRO-1 driver)" if args.zero1 else "")),
-                   "gemm_flops_per_step_per_gpu": flops_step,
-                   "gemm_tflops_per_s_whole_step": world * flops_step / (ms / 1e3) / 1e12,
-                   "l2": "not flushed: per-step working set ~3 GB >> 126 MB L2"},
+        "config": config,
+        "timing_mode": r["mode"],
         "tokens_per_s": world * T / (ms / 1e3),
-        "gpu_launches": launches,
-        "clocks": clocks.summary(),
+        "gemm_tflops_per_s_whole_step": world * flops_step / (ms / 1e3) / 1e12,
+        "gpu_launches": r["launches"],
+        "foreign_launches_per_step": r["foreign"],
+        "clocks": r["clocks"],
         "roofline": {"bound": "tensor", "kernel": "moss::gemm_mxf8_2cta_kernel (tcgen05.mma.cta_group::2 kind::mxf8f6f4.block_scale)",
                      "achieved": gemm_tflops, "peak": fp8_peak, "unit": "TFLOP/s", "frac": gemm_tflops / fp8_peak,
-                     "peak_source": "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (fp8 dense = 2x bf16)",
-                     "frac_of_burst": gemm_tflops / (2.0 * bf16_burst),
+                     "peak_source": peak_src,
+                     "frac_of_burst": gemm_tflops / roof["burst_tflops"] if have_roof else None,
                      "frac_of_nominal_4500": gemm_tflops / 4500.0, "traffic": traffic,
-                     "share_of_step": (g["ms"] / args.steps) / ms if g["launches"] else None},
+                     "share_of_step": (g["ms"] / steps) / ms if g["launches"] else None,
+                     "fp8_roof": roof},
         "kernels": {"quantize": rate("quant"), "amax": rate("amax"), "adamw_fp8": rate("adamw"),
                     "producers": rate("producer"),
-                    "gemm_ms_per_step": g["ms"] / args.steps, "all_kernels_ms_per_step": total_kernel_ms,
-                    "host_issue_ms_per_step": host_ms,
+                    "gemm_ms_per_step": g["ms"] / steps, "all_kernels_ms_per_step": total_kernel_ms,
+                    "host_issue_ms_per_step": r["host_ms"],
                     "timing_source": "per-kernel CUDA events from an instrumented eager pass of the same step "
                                      "(device sleep ahead of each step: no host gaps inside the events); "
-                                     "value/ms_per_step from " + ("CUDA-graph replays" if use_graph else "eager steps")},
+                                     "value/ms_per_step from " + r["mode"]},
         "e2e": e2e,
-        "memory": {"peak_allocated_gb": peak_gb,
+        "memory": {"peak_allocated_gb": r["peak_gb"],
                    "note": "torch.cuda.max_memory_allocated over warm-up, instrumented pass and timed steps"},
     }
-    if comm is not None:
-        line["collectives"] = {**comm, "note": "bucketed FP32 gradient all-reduce on the comm stream, events per "
-                                                "bucket over the instrumented steps (overlaps backward)"}
-    if not llama:
+    if r["comm"] is not None or comm_info is not None:
+        line["collectives"] = {**(r["comm"] or {}), "communicator": comm_info,
+                               "note": "bucketed FP32 gradient all-reduce on the comm stream, events per "
+                                       "bucket over the instrumented steps (overlaps backward)"}
+    if llama is not None:
+        line["llama7b"] = llama
+    if not llama_only:
         try:
             cmp = gemm_vs_cublas(dev, T)
         except Exception as ex:  # noqa: BLE001 - a library comparison must not sink the bench line
@@ -605,12 +831,11 @@ def main() -> None:
         except Exception as ex:  # noqa: BLE001
             line["kernels"]["quantize_standalone"] = {"error": str(ex)[:200]}
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_sample(1024, 4096)
+        line["cpu_baseline"] = cpu_sample(REF_SAMPLE["tokens"], REF_SAMPLE["d"])
         line["cpu_baseline"].pop("seconds", None)
-    if not llama and not args.no_llama and world == 1:
-        line["llama7b"] = llama7b_submeasure()
     print(json.dumps(line), flush=True)
-    if world > 1:
+    barrier()
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

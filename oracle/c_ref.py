@@ -36,6 +36,8 @@ def load():
     lib.moss_oracle_e4m3_sweep_compare.argtypes = [ctypes.c_uint32, ctypes.c_uint64, P]
     lib.moss_oracle_quant_two_level.restype = ctypes.c_int
     lib.moss_oracle_quant_two_level.argtypes = [P, I64, I64, P, P, P]
+    lib.moss_oracle_quant_two_level_rows.restype = ctypes.c_int
+    lib.moss_oracle_quant_two_level_rows.argtypes = [P, I64, I64, ctypes.c_float, P, P]
     lib.moss_oracle_encode_scaled.restype = I64
     lib.moss_oracle_encode_scaled.argtypes = [P, I64, ctypes.c_float, P]
     _lib = _Wrap(lib)
@@ -67,6 +69,35 @@ class _Wrap:
         st = self.lib.moss_oracle_quant_two_level(xf.ctypes.data, rows, cols, codes.ctypes.data,
                                                   micro.ctypes.data, g.ctypes.data)
         return codes, micro, float(g[0]), int(st)
+
+    def quant_two_level_mt(self, x, threads: int | None = None):
+        """quant_two_level with the per-block pass split over row ranges in
+        threads (ctypes releases the GIL); the amax is numpy's max|x| (exact),
+        g = f32(amax/448) as in the single-threaded function.  Same bits."""
+        from concurrent.futures import ThreadPoolExecutor
+        xf = np.ascontiguousarray(x, dtype=np.float32)
+        rows = int(np.prod(xf.shape[:-1])) if xf.ndim > 1 else 1
+        cols = xf.shape[-1]
+        if not np.isfinite(xf).all():
+            return None, None, 0.0, 1
+        amax = np.float32(np.abs(xf).max()) if xf.size else np.float32(0)
+        g = np.float32(amax / np.float32(448.0)) if amax > 0 else np.float32(1.0)
+        codes = np.empty(xf.shape, np.uint8)
+        micro = np.empty(xf.shape[:-1] + (cols // 32,), np.uint8)
+        n = max(1, min(threads or os.cpu_count(), rows))
+        cuts = [rows * i // n for i in range(n + 1)]
+        nb = cols // 32
+
+        def part(i):
+            r0, r1 = cuts[i], cuts[i + 1]
+            if r1 == r0:
+                return 0
+            return self.lib.moss_oracle_quant_two_level_rows(
+                xf.ctypes.data + r0 * cols * 4, r1 - r0, cols, float(g),
+                codes.ctypes.data + r0 * cols, micro.ctypes.data + r0 * nb)
+        with ThreadPoolExecutor(n) as ex:
+            st = max(ex.map(part, range(n)))
+        return codes, micro, float(g), int(st)
 
     def encode_scaled(self, w, scale: float):
         wf = np.ascontiguousarray(w, dtype=np.float32)

@@ -75,22 +75,11 @@ static int ceil_log2_ratio(float s, float g) {
     return e;                                         /* ms <= mg: ratio in (2^(e-1), 2^e] */
 }
 
-/* quantize.py:127-173, rows x cols f32 row-major, blocks of 32 along cols.
- * amax over the whole tensor is computed here.  Outputs: codes[rows*cols],
- * micro[rows*cols/32] (row-major), *g_out.  Returns 0, or 1 for non-finite
- * input, 2 for an E8M0 exponent below -127 (the reference raises). */
-int moss_oracle_quant_two_level(const float* x, int64_t rows, int64_t cols,
-                                uint8_t* codes, uint8_t* micro, float* g_out) {
+/* The per-block part of quantize.py:144-173 for rows x cols at a given
+ * global scale g (row ranges of one tensor can be done independently). */
+int moss_oracle_quant_two_level_rows(const float* x, int64_t rows, int64_t cols, float g,
+                                     uint8_t* codes, uint8_t* micro) {
     const int64_t nb = cols / 32;
-    float amax = 0.f;
-    for (int64_t i = 0; i < rows * cols; ++i) {
-        if (!isfinite(x[i])) return 1;
-        float a = fabsf(x[i]);
-        if (a > amax) amax = a;
-    }
-    float g = amax > 0.f ? amax / 448.0f : 1.0f;      /* == max_i f32(bmax_i/448) */
-    if (g == 0.f) g = 1.0f;
-    *g_out = g;
     int status = 0;
     for (int64_t r = 0; r < rows; ++r) {
         for (int64_t b = 0; b < nb; ++b) {
@@ -112,6 +101,24 @@ int moss_oracle_quant_two_level(const float* x, int64_t rows, int64_t cols,
         }
     }
     return status;
+}
+
+/* quantize.py:127-173, rows x cols f32 row-major, blocks of 32 along cols.
+ * amax over the whole tensor is computed here.  Outputs: codes[rows*cols],
+ * micro[rows*cols/32] (row-major), *g_out.  Returns 0, or 1 for non-finite
+ * input, 2 for an E8M0 exponent below -127 (the reference raises). */
+int moss_oracle_quant_two_level(const float* x, int64_t rows, int64_t cols,
+                                uint8_t* codes, uint8_t* micro, float* g_out) {
+    float amax = 0.f;
+    for (int64_t i = 0; i < rows * cols; ++i) {
+        if (!isfinite(x[i])) return 1;
+        float a = fabsf(x[i]);
+        if (a > amax) amax = a;
+    }
+    float g = amax > 0.f ? amax / 448.0f : 1.0f;      /* == max_i f32(bmax_i/448) */
+    if (g == 0.f) g = 1.0f;
+    *g_out = g;
+    return moss_oracle_quant_two_level_rows(x, rows, cols, g, codes, micro);
 }
 
 /* Weight copy at a given scale, train.py:113-118: codes = e4m3(f32(w)/f32(s)). */

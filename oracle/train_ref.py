@@ -25,7 +25,7 @@ def _deq2(a32: np.ndarray) -> np.ndarray:
     """deq(quant_two_level(a)) in float64; the C restatement (pinned to the
     numpy one and to the reference's golden vectors) does the quantization."""
     from . import c_ref
-    codes, micro, g, st = c_ref.load().quant_two_level(a32)
+    codes, micro, g, st = c_ref.load().quant_two_level_mt(a32)
     if st:
         raise ValueError("oracle quantization failed (non-finite or e8m0 range)")
     return R.dequantize_two_level(R.TwoLevel(codes, g, micro))
@@ -71,7 +71,9 @@ class OracleMossLinear(nn.Module):
         self.encode()
 
     def encode(self) -> None:
-        self.codes, _ = R.encode_weight(self.weight.detach().numpy(), self.sched.s_t)   # train.py:113-118
+        from . import c_ref        # == R.encode_weight bit for bit (tests/test_oracle.py)
+        self.codes, _ = c_ref.load().encode_scaled(self.weight.detach().numpy().astype(np.float32),
+                                                   np.float32(self.sched.s_t))   # train.py:113-118
 
     def w_deq(self) -> np.ndarray:
         return (R.fp8_decode(self.codes) * np.float32(self.sched.s_t)).astype(np.float64)
@@ -112,3 +114,54 @@ class OracleAdamW:
                 if R.rescale_due(layer.sched):
                     R.rescale(p.detach().numpy(), layer.sched)           # autoscale.py:86-96
                 layer.encode()                                           # next step's W codes
+
+
+def seeded_init(model, seed: int, std: float = 0.02) -> None:
+    """Device-independent initial parameters for a Llama model: parameter i
+    (named_parameters order) is N(0, std^2) from a CPU torch generator seeded
+    ``seed + i`` (1-D norm weights stay 1).  The GPU run and the CPU reference
+    both start from these values, so a committed reference curve can be
+    compared with a GPU run made later on another machine."""
+    with torch.no_grad():
+        for i, (_, p) in enumerate(model.named_parameters()):
+            if p.dim() == 1:
+                p.fill_(1.0)
+                continue
+            g = torch.Generator().manual_seed(seed + i)
+            val = torch.randn(tuple(p.shape), generator=g, dtype=torch.float32) * std
+            p.copy_(val.to(p.device, p.dtype))
+            layer = getattr(p, "oracle_layer", None)
+            if layer is not None:
+                layer.init_from(val.numpy())
+
+
+def reference_curve(cfg, *, steps: int, batch: int, seq: int, lr: float, warmup: int, data_seed: int,
+                    init_seed: int, active: int | None = None, log=None) -> list:
+    """The CPU float64 reference training run of ``cfg`` (a llama.LlamaConfig):
+    every linear is an OracleMossLinear, the optimizer is OracleAdamW with the
+    reference lr schedule (numpy_ref.lr_at = train.py:75-82), the data is
+    MarkovTokens(cfg.vocab, data_seed, active=active)."""
+    from paper_2511_05811_b200 import llama as L
+
+    L._LINEAR_FACTORY = lambda c, i, o, d: OracleMossLinear(i, o, c.interval)
+    try:
+        ref = L.LlamaModel(L.LlamaConfig(**{**cfg.__dict__, "compute_dtype": torch.float64, "moss": True,
+                                            "fused_ops": False}), device="cpu")
+    finally:
+        L._LINEAR_FACTORY = None
+    ref = ref.double()
+    seeded_init(ref, init_seed)
+    sched = lambda t: R.lr_at(t, lr_peak=lr, warmup=warmup, steps=steps)
+    opt = OracleAdamW(ref.named_parameters(), sched, 0.1, L.LlamaModel.no_decay)
+    data = L.MarkovTokens(cfg.vocab, seed=data_seed, active=active)
+    losses = []
+    for step in range(steps):
+        x, y = data.batch(batch, seq)
+        opt.zero_grad()
+        loss = ref(torch.as_tensor(x), torch.as_tensor(y))
+        loss.backward()
+        opt.step()
+        losses.append(float(loss))
+        if log is not None:
+            log(step, losses[-1])
+    return losses

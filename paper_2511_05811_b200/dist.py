@@ -43,12 +43,14 @@ class _Bucket:
 
 
 class GradBuckets:
-    def __init__(self, params, bucket_mb: float = 64.0, group=None):
+    def __init__(self, params, bucket_mb: float = 64.0, group=None, always_communicate: bool = False):
         if isinstance(params, nn.Module):
             params = list(params.parameters())
         self.params = [p for p in params if p.requires_grad]
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        # world 1 normally skips the collectives; tests force them (NCCL world 1 under graph capture)
+        self.communicate = self.world > 1 or (always_communicate and dist.is_initialized())
         dev = self.params[0].device
         self.cuda = dev.type == "cuda"
         self.comm_stream = torch.cuda.Stream(device=dev) if self.cuda else None
@@ -126,7 +128,7 @@ class GradBuckets:
         if b.launched:
             return
         b.launched = True
-        if self.world == 1:
+        if not self.communicate:
             return
         if self.cuda:
             ev = torch.cuda.Event()
@@ -152,7 +154,7 @@ class GradBuckets:
         for b in self.buckets:
             if b.work is not None:
                 b.work.wait()
-        if self.cuda and self.world > 1:
+        if self.cuda and self.communicate:
             torch.cuda.current_stream(self.buckets[0].buf.device).wait_stream(self.comm_stream)
 
     @property

@@ -449,16 +449,26 @@ class CudaGraphStep:
     """A whole training step (forward, backward, gradient exchange, fused
     optimizer kernels) captured once in a CUDA graph and replayed.
 
-    ``step_fn(*inputs) -> loss`` must run forward + backward (+ DP finish);
-    the optimizer's device half is captured after it.  Per replay the host
-    only runs ``opt.prepare()`` (O(1) per parameter + one H2D copy) and
-    ``graph.replay()``.  Steps that end with a rescale (every ``interval``
-    steps) run eagerly, exactly like the uncaptured path.
+    ``step_fn(*inputs) -> loss`` must run forward + backward; the gradient
+    exchange (``buckets``: dist.GradBuckets or zero.Zero1 — their NCCL
+    collectives are captured on the comm stream, which forks from and joins
+    the capture stream) and the optimizer's device half are captured after
+    it.  Per replay the host only runs ``prepare()`` (O(1) per parameter + one
+    H2D copy) and ``graph.replay()``.  Steps that end with a rescale (every
+    ``interval`` steps) run eagerly, exactly like the uncaptured path.
     """
 
-    def __init__(self, step_fn, opt: MossAdamW, static_inputs: tuple, zero_grad=None):
+    def __init__(self, step_fn, opt: MossAdamW, static_inputs: tuple, zero_grad=None, buckets=None):
         self.fn, self.opt, self.inputs = step_fn, opt, static_inputs
-        base = zero_grad or (lambda: opt.zero_grad(set_to_none=True))
+        self.buckets = buckets
+        if buckets is not None:
+            if getattr(buckets, "overlap_gather", False):
+                # a gather issued at the end of one replay and waited in the next
+                # forward would be a dependency between two graph launches
+                buckets.overlap_gather = False
+            base = zero_grad or buckets.reset
+        else:
+            base = zero_grad or (lambda: opt.zero_grad(set_to_none=True))
 
         def zero_all():
             base()
@@ -469,6 +479,20 @@ class CudaGraphStep:
         self.graph = None
         self.loss = None
 
+    def _fwd_bwd(self) -> torch.Tensor:
+        loss = self.fn(*self.inputs).detach()
+        if self.buckets is not None:
+            self.buckets.finish()
+        return loss
+
+    def _prepare(self) -> bool:
+        b = self.buckets
+        return b.prepare() if hasattr(b, "prepare") else self.opt.prepare()
+
+    def _launch(self, rescale: bool) -> None:
+        b = self.buckets
+        b.launch(rescale) if hasattr(b, "launch") else self.opt.launch(rescale)
+
     def _capture(self) -> None:
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
@@ -476,17 +500,18 @@ class CudaGraphStep:
         with torch.cuda.stream(s):
             for _ in range(2):                 # forward/backward only: no optimizer state change
                 self.zero_grad()
-                self.fn(*self.inputs).detach()
+                self._fwd_bwd()
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
-        self.zero_grad()
         with torch.cuda.graph(self.graph, stream=s):
-            # detached: the captured autograd graph (and the AccumulateGrad nodes bound to
+            # zeroing is part of the step: replays re-zero the bucket accumulators.
+            # detached loss: the captured autograd graph (and the AccumulateGrad nodes bound to
             # this capture stream) must not outlive the capture, or a later capture of
             # the same model on another stream picks up a cross-stream dependency
-            self.loss = self.fn(*self.inputs).detach()
-            self.opt.launch(False)
+            self.zero_grad()
+            self.loss = self._fwd_bwd()
+            self._launch(False)
         torch.cuda.current_stream().wait_stream(s)
 
     def __call__(self, *inputs) -> torch.Tensor:
@@ -497,12 +522,13 @@ class CudaGraphStep:
         if self.opt.rescale_due_next() or self.graph is None:
             # eager step (rescale, or the step before the first capture)
             self.zero_grad()
-            loss = self.fn(*self.inputs).detach()      # drop the eager autograd graph
-            self.opt.step()
+            loss = self._fwd_bwd()                    # detached: drop the eager autograd graph
+            self._launch(self._prepare())
             if self.graph is None:
                 self._capture()
             return loss
-        self.opt.prepare()
+        if self._prepare():
+            raise RuntimeError("rescale due inside a replayed step")     # rescale_due_next() said no
         self.graph.replay()
         return self.loss
 

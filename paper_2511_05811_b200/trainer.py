@@ -41,8 +41,9 @@ def make_optimizer(model: LlamaModel, lr: float, steps: int, warmup: int, weight
 def train(model: LlamaModel, data: MarkovTokens, *, steps: int, batch: int, seq: int, lr: float = 1e-3,
           warmup: int = 20, weight_decay: float = 0.1, buckets=None, divergence_threshold: float = 1e6,
           check_every: int = 1, cuda_graph: bool = False) -> TrainLog:
-    """``cuda_graph=True`` (single GPU) captures forward + backward + the
-    optimizer kernels once and replays the graph each step (nn.CudaGraphStep)."""
+    """``cuda_graph=True`` captures forward + backward + the gradient exchange
+    (``buckets``) + the optimizer kernels once and replays the graph each step
+    (nn.CudaGraphStep); rescale steps run eagerly."""
     opt = make_optimizer(model, lr, steps, warmup, weight_decay)
     if callable(buckets):                            # a factory: e.g. lambda opt: Zero1(opt)
         buckets = buckets(opt)
@@ -60,7 +61,8 @@ def train(model: LlamaModel, data: MarkovTokens, *, steps: int, batch: int, seq:
             loss = model(xt, yt)
             loss.backward()
             return loss
-        graphed = CudaGraphStep(fb, opt, (sx, sy))
+        # the gradient exchange (all-reduce buckets or ZeRO-1) is captured with the step
+        graphed = CudaGraphStep(fb, opt, (sx, sy), buckets=buckets)
     for step in range(steps):
         x, y = data.batch(batch, seq)
         xt = torch.as_tensor(x, device=dev)

@@ -242,9 +242,19 @@ class Zero1:
     # ------------------------------------------------------------------ step
     @torch.no_grad()
     def step(self, lr: float | None = None) -> None:
+        self.launch(self.prepare(lr))
+
+    def prepare(self, lr: float | None = None) -> bool:
+        """Host half of the step (schedule advance, staged kernel arguments);
+        True when this step rescales."""
         self.sync()                              # codes of the previous step must have landed
+        return self.opt.prepare(lr)
+
+    @torch.no_grad()
+    def launch(self, rescale: bool) -> None:
+        """Device half: replicated updates, K3 on this rank's slices, the FP8
+        all-gather (graph-capturable when not rescaling and not overlapped)."""
         opt = self.opt
-        rescale = opt.prepare(lr)
         opt.launch(rescale)                      # replicated parameters (sharded ones are skipped)
         local = set()
         for b in self.buckets:

@@ -229,3 +229,17 @@ def test_lr_schedule_matches_reference(mossq):
     for step in (0, 5, 99, 100, 500, 999):
         assert R.lr_at(step, lr_peak=0.01, warmup=100, steps=1000) == lr_at(cfg, step)
     assert math.isclose(R.lr_at(999, lr_peak=0.01, warmup=100, steps=1000), 0.001, rel_tol=0.01)
+
+
+def test_threaded_c_quantizer_equals_single_threaded():
+    """c_ref.quant_two_level_mt (row ranges in threads, used by the training
+    reference) gives the same codes / E8M0 / g as the single-threaded C path."""
+    from oracle import c_ref
+    lib = c_ref.load()
+    rng = np.random.default_rng(5)
+    for shape in [(1, 64), (7, 96), (256, 768), (1000, 2048)]:
+        x = (rng.standard_normal(shape) * rng.uniform(1e-3, 1e3)).astype(np.float32)
+        x[0, :32] = 0.0
+        a = lib.quant_two_level(x)
+        b = lib.quant_two_level_mt(x, threads=5)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2] and a[3] == b[3]

@@ -1,0 +1,14 @@
+#!/bin/bash
+# round 2, first box call: GPU tests, sanitizers, default bench
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/smi.txt
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/gputest.log 2>&1; echo "gputest rc=$?" >> gpurun_out/gputest.log
+for tool in memcheck racecheck synccheck; do
+  timeout 600 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize_kernels.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "rc=$?" >> gpurun_out/sanitize_$tool.log
+done
+timeout 900 python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+tail -c 3000 gpurun_out/gputest.log
+tail -3 gpurun_out/sanitize_*.log
+tail -c 1500 gpurun_out/bench.log
