@@ -491,9 +491,11 @@ def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: b
     if buckets is not None:
         opt.grad_scale = buckets.grad_scale
 
+    one = torch.ones((), device=dev, dtype=torch.float32)
+
     def fwd_bwd(xin):
         loss = fwd(xin)
-        loss.backward()
+        loss.backward(one)          # a resident seed gradient: no fill kernel per step
         return loss
 
     def step(xin):

@@ -39,6 +39,13 @@ enum moss_dtype { MOSS_F32 = 0, MOSS_BF16 = 1 };
 #define MOSS_FLAG_NONFINITE 1u      /* NaN/Inf input: quantize.py:88, fp8.py:139 */
 #define MOSS_FLAG_E8M0_RANGE 2u     /* e8m0 exponent < -127: fp8.py:219-222 */
 #define MOSS_FLAG_GRAD_NONFINITE 4u /* optim.py:89-90 */
+/* Any of these bits set when K3 starts => K3 skips its whole update (no
+ * write to w, m, v, codes or scale_out): the reference raises before it
+ * mutates anything (quantize.py:88, fp8.py:219-222, optim.py:89-90).  K3
+ * with p->step != 0 then also atomicMin()s p->step into flags[1], so a
+ * caller that passes step numbers must give K3 a TWO-word flags buffer,
+ * flags[1] initialised to 0xFFFFFFFF (= "no step skipped"). */
+#define MOSS_FLAG_SKIP_MASK (MOSS_FLAG_NONFINITE | MOSS_FLAG_E8M0_RANGE | MOSS_FLAG_GRAD_NONFINITE)
 
 /* Bytes of the tcgen05 block-scale-factor buffer for a rows x cols operand
  * (one E8M0 byte per 32 columns; 128-row x 4-block chunks of 512 B). */
@@ -125,7 +132,15 @@ typedef struct {
     float bc1, bc2;   /* 1 - beta1^t, 1 - beta2^t for the step being taken */
     int decoupled;    /* 1 = AdamW (decay on the old weight), 0 = L2 into g */
     float grad_scale; /* g is multiplied by this first (DP averaging, grad accumulation); 1 = none */
+    uint32_t step;    /* optimizer step number t (>= 1) recorded in flags[1] when the update is skipped; 0 = don't */
 } moss_adam_params;
+
+/* Sets `bit` in *flags if any of the n elements of x (f32 or bf16) is NaN/Inf.
+ * The optimizer runs it over the gradients K3's gate cannot vouch for (those
+ * not produced from flag-checked FP8 operands) BEFORE any K3 launch of the
+ * step, so a non-finite gradient skips every update of the step
+ * (optim.py:89-90 raises before mutating). */
+int moss_check_finite(const void* x, int dtype, int64_t n, uint32_t bit, uint32_t* flags, void* stream);
 
 /* moss_gemm_mxf8 with B given as stored [K, N] row-major (N contiguous) and unit
  * B scales: the dgrad product dX = dY W reads the per-tensor E4M3 weight codes
@@ -143,8 +158,10 @@ int moss_gemm_mxf8_bkn(const uint8_t* A, const uint8_t* SFA, const uint8_t* B_kn
  * w_fp8_t   [cols, rows] transposed codes for dgrad (nullable).
  * w_amax    device f32 max|w'| (nullable; memset by the call) — rescale input.
  * n_saturated  device u32 count of |w'| > enc_scale*448 (nullable).
- * Elements whose gradient is non-finite are left untouched and set
- * MOSS_FLAG_GRAD_NONFINITE (the reference raises before mutating). */
+ * If *flags has any MOSS_FLAG_SKIP_MASK bit set when the kernel starts, nothing
+ * is written (see MOSS_FLAG_SKIP_MASK).  Elements whose gradient is non-finite
+ * are left untouched and set MOSS_FLAG_GRAD_NONFINITE (a gradient that was not
+ * checked by moss_check_finite first: the rest of that launch still updates). */
 int moss_adamw_fp8(float* w, const void* g, int g_dtype, float* m, float* v, int64_t rows, int64_t cols,
                    const moss_adam_params* p, float enc_scale, uint8_t* w_fp8, uint8_t* w_fp8_t,
                    float* w_amax, uint32_t* n_saturated, uint32_t* flags, void* stream);
@@ -190,13 +207,14 @@ int moss_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q
  * mode 0 sum3:   out [T, d] = x[:, 0:d] + x[:, d:2d] + x[:, 2d:3d]   (x [T, 3d])
  * mode 1 bcast3: out [T, 3d] = [x, x, x]                              (x [T, d])
  * mode 2 add:    out = x + y
- * mode 3 scale:  out = x * (*scale)                                    (scale: device f32) */
-int moss_glue(int mode, const void* x, const void* y, const float* scale, void* out, float* amax, int64_t T,
-              int64_t d, void* stream);
-/* *acc = sum x^2 (f32) over n bf16 elements (n % 8 == 0); deterministic (fixed-order
- * reduction through `partials`, MOSS_SUMSQ_PARTIALS floats of caller scratch) */
+ * mode 3 scale:  out = x * f32(*scale * alpha)                         (scale: device f32, e.g. the
+ *                incoming loss gradient; alpha: host factor, e.g. 2/n for mean(y^2)) */
+int moss_glue(int mode, const void* x, const void* y, const float* scale, float alpha, void* out, float* amax,
+              int64_t T, int64_t d, void* stream);
+/* *acc = scale * sum x^2 (f32) over n bf16 elements (n % 8 == 0; scale = 1/n gives the mean);
+ * deterministic (fixed-order reduction through `partials`, MOSS_SUMSQ_PARTIALS floats of caller scratch) */
 #define MOSS_SUMSQ_PARTIALS 1024
-int moss_sumsq(const void* x, int64_t n, float* acc, float* partials, void* stream);
+int moss_sumsq(const void* x, int64_t n, float scale, float* acc, float* partials, void* stream);
 /* Cross entropy of bf16 logits [T, V] (V % 8 == 0) against int64 targets:
  * fwd  lse[t] = logsumexp(x[t, :]) (f32, one read of the row), loss[t] = lse[t] - x[t, y_t]
  * bwd  dlogits = (softmax(x) - onehot(y)) * (*scale), bf16; scale a device f32 (dL/dmean / T) */
@@ -208,10 +226,6 @@ int moss_cross_entropy_bwd(const void* logits, const int64_t* targets, const flo
 int moss_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
                   float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, void* stream);
 
-/* dst [cols, rows] = src [rows, cols]^T, u8 (E4M3 codes).  ZeRO-1 rebuilds
- * the dgrad operand W_fp8^T locally after the FP8 all-gather of W_fp8
- * (per-tensor codes commute with the transpose).  rows, cols % 16 == 0. */
-int moss_transpose_u8(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Per-group (COAT-style) comparator — NOT the MOSS path; the ablation the

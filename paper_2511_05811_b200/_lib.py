@@ -26,7 +26,7 @@ MOSS_BF16 = 1
 
 class AdamParams(ctypes.Structure):
     _fields_ = [("lr", _F), ("beta1", _F), ("beta2", _F), ("eps", _F), ("weight_decay", _F),
-                ("bc1", _F), ("bc2", _F), ("decoupled", _I), ("grad_scale", _F)]
+                ("bc1", _F), ("bc2", _F), ("decoupled", _I), ("grad_scale", _F), ("step", ctypes.c_uint32)]
 
 
 _SIGS = {
@@ -44,16 +44,16 @@ _SIGS = {
     "moss_swiglu_bwd": (_I, [_P, _P, _P, _P, _I64, _I64, _P]),
     "moss_rope_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
     "moss_rope_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
-    "moss_transpose_u8": (_I, [_P, _P, _I64, _I64, _P]),
     "moss_cross_entropy_fwd": (_I, [_P, _P, _P, _P, _I64, _I64, _P]),
-    "moss_glue": (_I, [_I, _P, _P, _P, _P, _P, _I64, _I64, _P]),
+    "moss_glue": (_I, [_I, _P, _P, _P, _F, _P, _P, _I64, _I64, _P]),
     "moss_gemm_mxf8_bkn": (_I, [_P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _P]),
-    "moss_sumsq": (_I, [_P, _I64, _P, _P, _P]),
+    "moss_sumsq": (_I, [_P, _I64, _F, _P, _P, _P]),
     "moss_cross_entropy_bwd": (_I, [_P, _P, _P, _P, _P, _I64, _I64, _P]),
     "moss_quant_per_group": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P, _P]),
     "moss_gemm_pergroup": (_I, [_P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _P]),
     "moss_encode_scaled": (_I, [_P, _I, _I64, _I64, _P, _F, _I, _P, _P, _P, _P, _P, _P]),
     "moss_gemm_mxf8": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _I, _P]),
+    "moss_check_finite": (_I, [_P, _I, _I64, ctypes.c_uint32, _P, _P]),
     "moss_adamw_fp8": (_I, [_P, _P, _I, _P, _P, _I64, _I64, ctypes.POINTER(AdamParams), _F, _P, _P, _P,
                             _P, _P, _P]),
     "moss_adamw_fp8_dev": (_I, [_P, _P, _I, _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
@@ -132,33 +132,46 @@ def sf_bytes(rows: int, cols: int) -> int:
     return int(lib().moss_sf_bytes(rows, cols))
 
 
+NO_STEP = 0xFFFFFFFF
+
+
 class FlagWord:
-    """A device u32 flag word (MOSS_FLAG_*) shared by a group of launches."""
+    """Device flag words shared by a group of launches: [0] the MOSS_FLAG_*
+    error bits, [1] the smallest optimizer step whose K3 update was skipped
+    because an error bit was already set (0xFFFFFFFF = none)."""
 
     def __init__(self, device=None):
-        self.t = torch.zeros(1, dtype=torch.int32, device=device or "cuda")
+        self.t = torch.tensor([0, -1], dtype=torch.int32, device=device or "cuda")
+        self._init = self.t.clone()
 
     @property
     def ptr(self) -> int:
         return self.t.data_ptr()
 
+    def read(self) -> tuple[int, int]:
+        """(error bits, first skipped step or NO_STEP) — one device sync."""
+        a, b = self.t.tolist()
+        return a & 0xFFFFFFFF, b & 0xFFFFFFFF
+
     def raise_if_set(self, where: str = "") -> None:
-        errors.raise_for_flags(int(self.t.item()), where)
+        errors.raise_for_flags(int(self.t[0].item()), where)
 
     def reset(self) -> None:
-        self.t.zero_()
+        self.t.copy_(self._init)
 
 
-_WS: dict[str, torch.Tensor] = {}
+_WS: dict[tuple[str, int], torch.Tensor] = {}
 
 
 def workspace(device) -> torch.Tensor:
-    """Per-device workspace of the fused quantizer (grid-barrier words), zeroed
-    once; every launch on it is ordered on the current stream."""
-    key = str(torch.device(device))
+    """Workspace of the fused quantizer (its grid-barrier words), one per
+    (device, stream), zeroed once: launches on one stream are ordered, and two
+    streams quantizing concurrently never share barrier words."""
+    dev = torch.device(device)
+    key = (str(dev), torch.cuda.current_stream(dev).cuda_stream)
     if key not in _WS:
         nbytes = int(lib().moss_workspace_bytes())
-        _WS[key] = torch.zeros((nbytes + 15) // 16 * 4, dtype=torch.int32, device=device)
+        _WS[key] = torch.zeros((nbytes + 15) // 16 * 4, dtype=torch.int32, device=dev)
     return _WS[key]
 
 
@@ -292,6 +305,13 @@ def adamw_fp8_dev(w, g, m, v, rows: int, cols: int, p_dev: int, enc_dev: int | N
               "moss_adamw_fp8_dev")
 
 
+def check_finite(x: torch.Tensor, flags: FlagWord, bit: int = 4) -> None:
+    """Set ``bit`` (default MOSS_FLAG_GRAD_NONFINITE) if x has a NaN/Inf."""
+    with _Span("check", x.numel() * x.element_size()):
+        check(lib().moss_check_finite(x.data_ptr(), dtype_code(x), x.numel(), bit, flags.ptr, stream()),
+              "moss_check_finite")
+
+
 def adamw_fp8(w, g, m, v, rows: int, cols: int, params: AdamParams, enc_scale: float, flags: FlagWord, *,
               w_fp8=None, w_fp8_t=None, w_amax=None, n_saturated=None) -> None:
     n = rows * cols
@@ -358,12 +378,6 @@ def rope_bwd(dq, dk, dv, cos, sin, dqkv, amax, B: int, S: int, H: int, hd: int) 
                                   dqkv.data_ptr(), ptr(amax), B, S, H, hd, stream()), "moss_rope_bwd")
 
 
-def transpose_u8(src: torch.Tensor, dst: torch.Tensor) -> None:
-    rows, cols = src.shape
-    with _Span("transpose", 2 * rows * cols):
-        check(lib().moss_transpose_u8(src.data_ptr(), dst.data_ptr(), rows, cols, stream()), "moss_transpose_u8")
-
-
 def quant_per_group(x2d, codes, scales, flags: FlagWord, group: int = 128) -> None:
     rows, cols = x2d.shape
     with _Span("quant_pg", rows * cols * (x2d.element_size() + 1)):
@@ -393,17 +407,19 @@ def cross_entropy_bwd(logits, targets, lse, scale, dlogits) -> None:
                                            dlogits.data_ptr(), T, V, stream()), "moss_cross_entropy_bwd")
 
 
-def glue(mode: int, x, out, amax, *, y=None, scale=None, T: int, d: int) -> None:
+def glue(mode: int, x, out, amax, *, y=None, scale=None, alpha: float = 1.0, T: int, d: int) -> None:
     with _Span("producer", T * d * (2 + (4 if mode in (0, 1) else 2) + (2 if mode == 2 else 0))):
-        check(lib().moss_glue(mode, x.data_ptr(), ptr(y), ptr(scale), out.data_ptr(), ptr(amax), T, d, stream()),
+        check(lib().moss_glue(mode, x.data_ptr(), ptr(y), ptr(scale), float(alpha), out.data_ptr(), ptr(amax), T, d,
+                              stream()),
               "moss_glue")
 
 
 SUMSQ_PARTIALS = 1024       # include/moss_b200.h MOSS_SUMSQ_PARTIALS
 
 
-def sumsq(x, acc) -> None:
-    """acc[0] = sum x^2 (f32, fixed-order: reproducible); acc must hold 1 + SUMSQ_PARTIALS floats
-    (the tail is the kernel's scratch)."""
+def sumsq(x, acc, scale: float = 1.0) -> None:
+    """acc[0] = scale * sum x^2 (f32, fixed-order: reproducible); acc must hold 1 + SUMSQ_PARTIALS
+    floats (the tail is the kernel's scratch)."""
     with _Span("producer", x.numel() * 2, kernels=2):
-        check(lib().moss_sumsq(x.data_ptr(), x.numel(), acc.data_ptr(), acc.data_ptr() + 4, stream()), "moss_sumsq")
+        check(lib().moss_sumsq(x.data_ptr(), x.numel(), float(scale), acc.data_ptr(), acc.data_ptr() + 4, stream()),
+              "moss_sumsq")

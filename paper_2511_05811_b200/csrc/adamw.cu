@@ -47,6 +47,12 @@ __global__ void __launch_bounds__(256) adamw_fp8_kernel(float* __restrict__ w, c
     // device-resident hyper-parameters (CUDA-graph replays): read them once per CTA
     if (p_dev) p = *p_dev;
     if (enc_dev) enc_scale = *enc_dev;
+    // error gate: an earlier kernel of this step flagged a non-finite / out-of-range
+    // value -> no update at all (the reference raises before mutating, optim.py:89-90)
+    if (*reinterpret_cast<volatile uint32_t*>(flags) & MOSS_FLAG_SKIP_MASK) {
+        if (p.step && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicMin(flags + 1, p.step);
+        return;
+    }
     if (scale_out && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *scale_out = enc_scale;
     __shared__ __align__(16) uint8_t ctile[TRANS ? AT_ROWS : 1][AT_COLS];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -149,6 +155,33 @@ __global__ void __launch_bounds__(256) adamw_fp8_kernel(float* __restrict__ w, c
         if (lane == 0 && sat) atomicAdd(nsat, sat);
     }
     if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(flags, MOSS_FLAG_GRAD_NONFINITE);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) check_finite_kernel(const T* __restrict__ x, int64_t n, uint32_t bit,
+                                                           uint32_t* flags) {
+    bool bad = false;
+    const int64_t n8 = n / 8;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+        float v[8];
+        Vec8<T>::load(x + i * 8, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bad |= nonfinite(v[j]);
+    }
+    for (int64_t i = n8 * 8 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        bad |= nonfinite(static_cast<float>(x[i]));
+    if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, bit);
+}
+
+int launch_check_finite(const void* x, int dtype, int64_t n, uint32_t bit, uint32_t* flags, cudaStream_t st) {
+    if (n <= 0) return MOSS_OK;
+    const int64_t want = (n / 8 + 255) / 256;
+    const int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), 148 * 8);
+    if (dtype == MOSS_BF16)
+        check_finite_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, n, bit, flags);
+    else
+        check_finite_kernel<float><<<grid, 256, 0, st>>>((const float*)x, n, bit, flags);
+    return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 
 template <typename GT>

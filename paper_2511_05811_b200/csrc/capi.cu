@@ -25,6 +25,7 @@ int launch_adamw(float* w, const void* g, int g_dtype, float* m, float* v, int64
                  const moss_adam_params& p, float enc_scale, const moss_adam_params* p_dev, const float* enc_dev,
                  float* scale_out, uint8_t* w_fp8, uint8_t* w_fp8_t, float* w_amax, uint32_t* nsat,
                  uint32_t* flags, cudaStream_t st);
+int launch_check_finite(const void* x, int dtype, int64_t n, uint32_t bit, uint32_t* flags, cudaStream_t st);
 int launch_rmsnorm_fwd(const void* x, const void* delta, void* x_out, const float* w, float eps, void* y, float* rstd,
                        float* amax, int64_t T, int64_t d, cudaStream_t st);
 int launch_rmsnorm_bwd(const void* dy, const void* x, const float* w, const float* rstd, const void* d_res, void* dx,
@@ -36,10 +37,9 @@ int launch_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void*
                     int64_t S, int64_t H, int64_t hd, cudaStream_t st);
 int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
                     float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, cudaStream_t st);
-int launch_transpose_u8(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, cudaStream_t st);
-int launch_glue(int mode, const void* x, const void* y, const float* scale, void* out, float* amax, int64_t T,
-                int64_t d, cudaStream_t st);
-int launch_sumsq(const void* x, int64_t n, float* acc, float* parts, cudaStream_t st);
+int launch_glue(int mode, const void* x, const void* y, const float* scale, float alpha, void* out, float* amax,
+                int64_t T, int64_t d, cudaStream_t st);
+int launch_sumsq(const void* x, int64_t n, float scale, float* acc, float* parts, cudaStream_t st);
 int launch_xent_fwd(const void* logits, const int64_t* targets, float* lse, float* loss, int64_t T, int64_t V,
                     cudaStream_t st);
 int launch_xent_bwd(const void* logits, const int64_t* targets, const float* lse, const float* scale, void* dlogits,
@@ -180,6 +180,13 @@ int moss_adamw_fp8_dev(float* w, const void* g, int g_dtype, float* m, float* v,
                               w_fp8_t, w_amax, n_saturated, flags, (cudaStream_t)stream);
 }
 
+int moss_check_finite(const void* x, int dtype, int64_t n, uint32_t bit, uint32_t* flags, void* stream) {
+    if (n < 0) return MOSS_ERR_SHAPE;
+    if (!x || !flags || !dtype_ok(dtype) || !bit) return MOSS_ERR_ARGUMENT;
+    if (!aligned(x, 16)) return MOSS_ERR_ALIGN;
+    return moss::launch_check_finite(x, dtype, n, bit, flags, (cudaStream_t)stream);
+}
+
 // ---------------------------------------------------------------- producer kernels (bf16)
 static inline bool al16(const void* p) { return p == nullptr || aligned(p, 16); }
 
@@ -235,26 +242,19 @@ int moss_rope_bwd(const void* dq, const void* dk, const void* dv, const float* c
     return moss::launch_rope_bwd(dq, dk, dv, cosv, sinv, dqkv, amax, B, S, H, hd, (cudaStream_t)stream);
 }
 
-int moss_transpose_u8(const uint8_t* src, uint8_t* dst, int64_t rows, int64_t cols, void* stream) {
-    if (rows <= 0 || cols <= 0 || rows > 65535 * 64LL) return MOSS_ERR_SHAPE;
-    if (!src || !dst) return MOSS_ERR_ARGUMENT;
-    if (!aligned(src, 16) || !aligned(dst, 16) || cols % 16 || rows % 16) return MOSS_ERR_ALIGN;
-    return moss::launch_transpose_u8(src, dst, rows, cols, (cudaStream_t)stream);
-}
-
-int moss_glue(int mode, const void* x, const void* y, const float* scale, void* out, float* amax, int64_t T,
-              int64_t d, void* stream) {
+int moss_glue(int mode, const void* x, const void* y, const float* scale, float alpha, void* out, float* amax,
+              int64_t T, int64_t d, void* stream) {
     if (T <= 0 || d <= 0 || d % 8 || mode < 0 || mode > 3) return mode < 0 || mode > 3 ? MOSS_ERR_ARGUMENT : MOSS_ERR_SHAPE;
     if (!x || !out || (mode == 2 && !y) || (mode == 3 && !scale)) return MOSS_ERR_ARGUMENT;
     if (!al16(x) || !al16(y) || !al16(out)) return MOSS_ERR_ALIGN;
-    return moss::launch_glue(mode, x, y, scale, out, amax, T, d, (cudaStream_t)stream);
+    return moss::launch_glue(mode, x, y, scale, alpha, out, amax, T, d, (cudaStream_t)stream);
 }
 
-int moss_sumsq(const void* x, int64_t n, float* acc, float* partials, void* stream) {
+int moss_sumsq(const void* x, int64_t n, float scale, float* acc, float* partials, void* stream) {
     if (n <= 0 || n % 8) return MOSS_ERR_SHAPE;
     if (!x || !acc || !partials) return MOSS_ERR_ARGUMENT;
     if (!al16(x)) return MOSS_ERR_ALIGN;
-    return moss::launch_sumsq(x, n, acc, partials, (cudaStream_t)stream);
+    return moss::launch_sumsq(x, n, scale, acc, partials, (cudaStream_t)stream);
 }
 
 int moss_cross_entropy_fwd(const void* logits, const int64_t* targets, float* lse, float* loss, int64_t T, int64_t V,

@@ -243,12 +243,8 @@ static int launch_gemm_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B,
                          cudaStream_t st) {
     using L = GemmLayout<BN, STAGES>;
     auto kern = gemm_mxf8_kernel<BN, STAGES, OUT_BF16>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM) != cudaSuccess)
-            return MOSS_ERR_CUDA;
-        attr_set = true;
-    }
+    static bool attr_set[kMaxDevices] = {};
+    if (!smem_optin(kern, L::SMEM, attr_set)) return MOSS_ERR_CUDA;
     CUtensorMap ta, tb;
     if (!make_kmajor_map(&ta, A, M, K, G_BM) || !make_kmajor_map(&tb, B, N, K, BN)) return MOSS_ERR_CUDA;
     const int sms = sm_count();

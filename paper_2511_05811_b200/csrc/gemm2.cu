@@ -438,12 +438,8 @@ static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B
                           cudaStream_t st) {
     using L = G2Layout<STAGES, TMA_EPI, EPI_WARPS, BN>;
     auto kern = gemm_mxf8_2cta_kernel<OUT_BF16, STAGES, TMA_EPI, EPI_WARPS, BN, B_MN>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM) != cudaSuccess)
-            return MOSS_ERR_CUDA;
-        attr_set = true;
-    }
+    static bool attr_set[kMaxDevices] = {};
+    if (!smem_optin(kern, L::SMEM, attr_set)) return MOSS_ERR_CUDA;
     CUtensorMap ta, tb, tsa, tsb, td;
     const int64_t sfa_rows = ((M + 127) / 128) * (K / 128) * 2;
     const int64_t sfb_rows = ((N + 127) / 128) * (K / 128) * 2;

@@ -36,15 +36,39 @@ inline bool make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, size_t ele
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Launcher state that the CUDA runtime keeps per device (the shared-memory
+// opt-in of cudaFuncSetAttribute, occupancy, SM count) is cached per device:
+// one process may drive several GPUs.  (Occupancy of kernels without a
+// dynamic shared-memory opt-in depends only on the kernel and the arch; those
+// caches stay per process on this one-arch (sm_100a) build.)
+constexpr int kMaxDevices = 64;
+
+inline int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return (dev >= 0 && dev < kMaxDevices) ? dev : 0;
+}
+
 inline int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+    static int n[kMaxDevices] = {};
+    const int dev = current_device();
+    if (!n[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        n[dev] = v > 0 ? v : 148;
     }
-    return n;
+    return n[dev];
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device);
+// `done` is the caller's per-kernel static table
+template <typename K>
+inline bool smem_optin(K kern, int bytes, bool (&done)[kMaxDevices]) {
+    const int dev = current_device();
+    if (done[dev]) return true;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+    done[dev] = true;
+    return true;
 }
 
 }  // namespace moss

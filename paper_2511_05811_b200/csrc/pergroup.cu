@@ -280,12 +280,8 @@ int launch_gemm_pergroup(const uint8_t* A, const float* sa_t, const uint8_t* B, 
         return MOSS_ERR_CUDA;
     const bool bf = d_dtype == MOSS_BF16;
     auto kern = bf ? gemm_pergroup_kernel<true> : gemm_pergroup_kernel<false>;
-    static bool attr[2] = {false, false};
-    if (!attr[bf]) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PgLayout::SMEM) != cudaSuccess)
-            return MOSS_ERR_CUDA;
-        attr[bf] = true;
-    }
+    static bool attr[2][kMaxDevices] = {};
+    if (!smem_optin(kern, PgLayout::SMEM, attr[bf])) return MOSS_ERR_CUDA;
     const int64_t tiles = (M / PG_BM) * (N / PG_BN);
     const int grid = (int)std::min<int64_t>(tiles, sm_count());
     kern<<<grid, PG_THREADS, PgLayout::SMEM, st>>>(ta, tb, sa_t, sb_t, D, ldd, (int)M, (int)N, (int)K);

@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(256) rope_bwd_kernel(const __nv_bfloat16* __re
 // mode 0: sum3   out [T, d] = a + b + c from x [T, 3d] (column blocks), amax(out)
 // mode 1: bcast3 out [T, 3d] = [x, x, x] from x [T, d],               amax(x)
 // mode 2: add    out [T, d] = x + y,                                  amax(out)
-// mode 3: mse'   out [T, d] = x * (*scale),                           amax(out)   (dL/dy of mean(y^2): scale = 2 g / n)
+// mode 3: mse'   out [T, d] = x * f32(*scale * alpha),                amax(out)   (dL/dy of mean(y^2): *scale = g, alpha = 2/n)
 // Each thread owns 8 columns and walks rows with stride gridDim.y, GLUE_R rows
 // per iteration: all 16-byte loads of the R rows are issued before any math
 // (memory-level parallelism; one row per iteration left the 2-input add at
@@ -456,12 +456,13 @@ constexpr int GLUE_R = 4;
 template <int MODE>
 __global__ void __launch_bounds__(256) glue_kernel(const __nv_bfloat16* __restrict__ x,
                                                    const __nv_bfloat16* __restrict__ y, const float* __restrict__ scale,
-                                                   __nv_bfloat16* __restrict__ out, uint32_t* amax, int64_t T, int d) {
+                                                   float alpha, __nv_bfloat16* __restrict__ out, uint32_t* amax,
+                                                   int64_t T, int d) {
     constexpr int NIN = MODE == 0 ? 3 : MODE == 2 ? 2 : 1;
     __shared__ uint32_t red_u[8];
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
     uint32_t m = 0;
-    const float sc = MODE == 3 ? *scale : 0.f;
+    const float sc = MODE == 3 ? *scale * alpha : 0.f;
     const int64_t in_ld = MODE == 0 ? 3 * (int64_t)d : d;
     const int64_t out_ld = MODE == 1 ? 3 * (int64_t)d : d;
     if (c < d) {
@@ -528,11 +529,11 @@ __global__ void __launch_bounds__(256) sumsq_kernel(const __nv_bfloat16* __restr
 }
 
 __global__ void __launch_bounds__(SUMSQ_PARTS) sumsq_final_kernel(const float* __restrict__ parts, int n,
-                                                                  float* __restrict__ acc) {
+                                                                  float scale, float* __restrict__ acc) {
     __shared__ float red[SUMSQ_PARTS / 32];
     float v = threadIdx.x < n ? parts[threadIdx.x] : 0.f;
     v = block_sum<SUMSQ_PARTS>(v, red);
-    if (threadIdx.x == 0) *acc = v;
+    if (threadIdx.x == 0) *acc = v * scale;
 }
 
 // ------------------------------------------------------------------ cross entropy (LM head)
@@ -731,8 +732,8 @@ int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float*
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 
-int launch_glue(int mode, const void* x, const void* y, const float* scale, void* out, float* amax, int64_t T,
-                int64_t d, cudaStream_t st) {
+int launch_glue(int mode, const void* x, const void* y, const float* scale, float alpha, void* out, float* amax,
+                int64_t T, int64_t d, cudaStream_t st) {
     if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
     const int64_t gx = (d / 8 + 255) / 256;
     auto kern = mode == 0 ? glue_kernel<0> : mode == 1 ? glue_kernel<1> : mode == 2 ? glue_kernel<2> : glue_kernel<3>;
@@ -741,16 +742,16 @@ int launch_glue(int mode, const void* x, const void* y, const float* scale, void
     const int64_t gy = std::min<int64_t>((T + GLUE_R - 1) / GLUE_R,
                                          std::max<int64_t>(1, (int64_t)sm_count() * occ[mode] / gx));
     kern<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)y, scale,
-                                                           (__nv_bfloat16*)out, reinterpret_cast<uint32_t*>(amax), T,
+                                                           alpha, (__nv_bfloat16*)out, reinterpret_cast<uint32_t*>(amax), T,
                                                            (int)d);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 
-int launch_sumsq(const void* x, int64_t n, float* acc, float* parts, cudaStream_t st) {
+int launch_sumsq(const void* x, int64_t n, float scale, float* acc, float* parts, cudaStream_t st) {
     const int64_t nvec = n / 8;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nvec + 255) / 256, SUMSQ_PARTS));
     sumsq_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, nvec, parts);
-    sumsq_final_kernel<<<1, SUMSQ_PARTS, 0, st>>>(parts, grid, acc);
+    sumsq_final_kernel<<<1, SUMSQ_PARTS, 0, st>>>(parts, grid, scale, acc);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 

@@ -257,9 +257,6 @@ static void launch_quant_t(const T* x, int64_t rows, int64_t cols, const float* 
                                                                micro_t, g_out, flags);
 }
 
-bool launch_quant_v3(const void* x, int64_t rows, int64_t cols, const float* amax, uint8_t* codes, uint8_t* sf,
-                     uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t, float* g_out,
-                     uint32_t* flags, cudaStream_t st);
 bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int amax_given, uint8_t* codes,
                      uint8_t* sf, uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t, float* g_out,
                      uint32_t* ws, uint32_t* flags, cudaStream_t st, int* status);
@@ -267,9 +264,11 @@ bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int
 int launch_quant_mx2(const void* x, int dtype, int64_t rows, int64_t cols, const float* amax, uint8_t* codes,
                      uint8_t* sf, uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t, float* g_out,
                      uint32_t* flags, cudaStream_t st) {
-    if (dtype == MOSS_BF16 &&
-        launch_quant_v3(x, rows, cols, amax, codes, sf, micro, codes_t, sf_t, micro_t, g_out, flags, st))
-        return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+    int status = MOSS_OK;
+    // the TMA-tiled kernel in its given-amax mode (reads *amax, never writes it)
+    if (dtype == MOSS_BF16 && launch_quant_v4(x, rows, cols, const_cast<float*>(amax), 1, codes, sf, micro, codes_t,
+                                              sf_t, micro_t, g_out, nullptr, flags, st, &status))
+        return status;
     if (dtype == MOSS_BF16)
         launch_quant_t((const __nv_bfloat16*)x, rows, cols, amax, codes, sf, micro, codes_t, sf_t, micro_t, g_out,
                        flags, st);

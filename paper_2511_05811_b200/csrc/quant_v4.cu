@@ -474,7 +474,8 @@ bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int
                                   quant_mx2_v4_kernel<false, true, true>,  quant_mx2_v4_kernel<true, false, true>};
     const int ki = (row && col ? 0 : (col ? 1 : 2)) + (mic ? 3 : 0);
     const KT kern = kernels[ki];
-    static int occ[6] = {0, 0, 0, 0, 0, 0};
+    static int occ_dev[kMaxDevices][6] = {};
+    int* occ = occ_dev[current_device()];
     if (!occ[ki]) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q4_SMEM) != cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[ki], kern, Q4_THREADS, Q4_SMEM) != cudaSuccess ||

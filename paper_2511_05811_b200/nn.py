@@ -267,7 +267,8 @@ class MossAdamW:
     updated weights on the host and run eagerly (``launch(rescale=True)``).
     """
 
-    _WORDS = 12            # moss_adam_params (9 words) + enc scale (word 9), padded to 48 B
+    _WORDS = 12            # moss_adam_params (10 words, word 9 = step) + enc scale (word 10), padded to 48 B
+    _ENC = 10
     _RING = 8
 
     def __init__(self, params: Iterable[nn.Parameter] | nn.Module, lr: float = 3e-4,
@@ -298,7 +299,15 @@ class MossAdamW:
         self.t = 0
         self.grad_scale = 1.0
         dev = self.params[0].device
-        self.state = {id(p): (torch.zeros_like(p), torch.zeros_like(p)) for p in self.params}
+        intervals = {p.moss_layer.interval for p in self.params if hasattr(p, "moss_layer")}
+        if len(intervals) > 1:
+            # one rescale cadence per optimizer: rescale steps run eagerly and
+            # CudaGraphStep decides eager-vs-replay from it (autoscale.py:82-96)
+            raise InvalidArgumentError(f"MossLinear layers of one optimizer must share the rescale interval, "
+                                       f"got {sorted(intervals)}")
+        # moments are allocated at the first update (lazily), so parameters handed to
+        # a sharded driver (zero.Zero1.shard) never hold full-size m, v
+        self.state: dict[int, tuple | None] = {id(p): None for p in self.params}
         self.index = {id(p): i for i, p in enumerate(self.params)}
         self.sharded: set[int] = set()      # parameters whose update is done elsewhere (zero.Zero1)
         self.saturations = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -309,6 +318,9 @@ class MossAdamW:
         self._ring_events: list = [None] * self._RING
         self._slot = 0
         self._rescale_pending = False
+        # host state before each step prepared since the last clean check():
+        # restored when a device error gate skipped that step's update
+        self._snapshots: dict[int, tuple] = {}
 
     def shard(self, params) -> None:
         """Hand the update of ``params`` to a sharded driver (zero.Zero1): their
@@ -321,6 +333,22 @@ class MossAdamW:
     def record_ptr(self, p) -> int:
         """Device address of p's staged kernel arguments (moss_adam_params + encode scale)."""
         return self.hp_dev.data_ptr() + self.index[id(p)] * self._WORDS * 4
+
+    def enc_ptr(self, p) -> int:
+        """Device address of p's staged encode scale f32(s_{t+1})."""
+        return self.record_ptr(p) + self._ENC * 4
+
+    def _moss_layers(self):
+        return [p.moss_layer for p in self.params if hasattr(p, "moss_layer")]
+
+    def _snapshot(self) -> tuple:
+        return (self.t, [(l.schedule.s_t, l.schedule.t, l.schedule.last_rescale_step) for l in self._moss_layers()])
+
+    def _restore(self, snap: tuple) -> None:
+        self.t = snap[0]
+        for layer, (s_t, t, last) in zip(self._moss_layers(), snap[1]):
+            layer.schedule.s_t, layer.schedule.t, layer.schedule.last_rescale_step = s_t, t, last
+        self._rescale_pending = False
 
     def zero_grad(self, set_to_none: bool = True) -> None:
         for p in self.params:
@@ -347,6 +375,9 @@ class MossAdamW:
     def prepare(self, lr: float | None = None) -> bool:
         """Host half of a step; returns True when this step must rescale (eager launch)."""
         eta = self.current_lr() if lr is None else lr
+        self._snapshots[self.t + 1] = self._snapshot()
+        if len(self._snapshots) > 1024:                # never checked: keep the recent ones
+            self._snapshots.pop(min(self._snapshots))
         self.t += 1
         b1, b2 = self.betas
         bc1, bc2 = 1.0 - b1 ** self.t, 1.0 - b2 ** self.t
@@ -365,6 +396,7 @@ class MossAdamW:
         buf[:, 6] = bc2
         ibuf[:, 7] = int(self.decoupled)
         buf[:, 8] = self.grad_scale
+        ibuf[:, 9] = self.t                                    # recorded by K3 if its error gate skips
         rescale = False
         for i, p in enumerate(self.params):
             buf[i, 4] = self.wd_of[id(p)]
@@ -373,7 +405,7 @@ class MossAdamW:
                 sched = layer.schedule
                 auto_scale_advance(sched, eta)                 # O(1), autoscale.py:71-79
                 rescale |= rescale_due(sched)
-                buf[i, 9] = np.float32(sched.s_t)
+                buf[i, self._ENC] = np.float32(sched.s_t)
         self.hp_dev.copy_(self.hp_pinned[slot], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
@@ -387,6 +419,15 @@ class MossAdamW:
         rescale = self._rescale_pending if rescale is None else rescale
         base = self.hp_dev.data_ptr()
         stride = self._WORDS * 4
+        # gradients the error gate cannot vouch for — not made by an FP8 GEMM from
+        # flag-checked operands — are checked BEFORE any update of the step, so a
+        # non-finite one skips every K3 launch (optim.py:89-90 raises before mutating)
+        for p in self.params:
+            layer = getattr(p, "moss_layer", None)
+            if layer is None and p.grad is not None:
+                _lib.check_finite(p.grad, device_flags(p.device))
+            elif layer is not None and not layer.fp8_backward and getattr(p, "main_grad", None) is not None:
+                _lib.check_finite(p.main_grad, device_flags(p.device))
         for i, p in enumerate(self.params):
             if id(p) in self.sharded:
                 continue
@@ -394,7 +435,10 @@ class MossAdamW:
             g = p.main_grad if layer is not None else p.grad
             if g is None:
                 continue
-            m, v = self.state[id(p)]
+            st = self.state[id(p)]
+            if st is None:
+                st = self.state[id(p)] = (torch.zeros_like(p), torch.zeros_like(p))
+            m, v = st
             flags = device_flags(p.device)
             p_dev = base + i * stride
             if layer is None:
@@ -405,7 +449,8 @@ class MossAdamW:
             if rescale:
                 _lib.adamw_fp8_dev(p.data, g, m, v, rows, cols, p_dev, None, flags, w_amax=layer.w_amax)
             else:
-                _lib.adamw_fp8_dev(p.data, g, m, v, rows, cols, p_dev, p_dev + 36, flags, scale_out=layer.w_scale,
+                _lib.adamw_fp8_dev(p.data, g, m, v, rows, cols, p_dev, p_dev + self._ENC * 4, flags,
+                                   scale_out=layer.w_scale,
                                    w_fp8=layer.w_fp8, w_amax=layer.w_amax,
                                    n_saturated=self.saturations)
         if rescale:
@@ -413,12 +458,16 @@ class MossAdamW:
 
     def _finish_rescale(self) -> None:
         """JIT snap of every MOSS scale to max|W'|/448 and re-encode (autoscale.py:86-96)."""
-        for p in self.params:
-            layer = getattr(p, "moss_layer", None)
-            if layer is None or id(p) in self.sharded:
-                continue
+        self.check("rescale step")          # a gated (skipped) update leaves no amax to snap to
+        mine = [p for p in self.params if hasattr(p, "moss_layer") and id(p) not in self.sharded]
+        if not mine:
+            self._rescale_pending = False
+            return
+        # every layer's max|W'| in ONE device->host read (not one sync per layer)
+        amaxes = torch.cat([p.moss_layer.w_amax.view(1) for p in mine]).cpu().tolist()
+        for p, amax in zip(mine, amaxes):
+            layer = p.moss_layer
             sched = layer.schedule
-            amax = float(layer.w_amax.item())
             sched.s_t = amax / E4M3.max_value if amax > 0 else 1.0
             sched.last_rescale_step = sched.t
             self.rescale_events.append((self.t, id(p)))
@@ -429,10 +478,27 @@ class MossAdamW:
         self.launch(self.prepare(lr))
 
     def check(self, where: str = "MossAdamW") -> None:
-        """Raise pending device-side errors (non-finite grads/activations, E8M0 range)."""
-        devs = {str(p.device) for p in self.params}
-        for d in devs:
-            raise_if_flagged(d, where)
+        """Raise pending device-side errors (non-finite grads/activations, E8M0 range).
+
+        The error gate in K3 skipped every update from the first flagged step
+        on, so before raising, the host half (step counter, scale schedules)
+        is rolled back to its state before that step: host and device agree
+        and the optimizer is exactly as it was after the last good step."""
+        first = None
+        bad = []
+        for d in sorted({str(p.device) for p in self.params}):
+            bits, skipped = device_flags(d).read()
+            if bits:
+                bad.append(d)
+                if skipped != _lib.NO_STEP:
+                    first = skipped if first is None else min(first, skipped)
+        if bad:
+            if first is not None and first in self._snapshots:
+                self._restore(self._snapshots[first])
+            self._snapshots.clear()
+            for d in bad:
+                raise_if_flagged(d, where)
+        self._snapshots.clear()
 
     def dominance_violations(self) -> int:
         """s_auto < s_jit count over MOSS weights right now (train.py:163-167); syncs."""

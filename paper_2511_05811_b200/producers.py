@@ -48,10 +48,13 @@ class RMSNormFn(torch.autograd.Function):
         ctx.save_for_backward(x2, weight, rstd)
         ctx.consumer, ctx.shape = consumer, x.shape
         ctx.mark_non_differentiable(amax)
+        ctx.set_materialize_grads(False)     # no zero-filled gradient for the amax output
         return y.view(x.shape), amax
 
     @staticmethod
     def backward(ctx, dy, _damax):
+        if dy is None:
+            return None, None, None, None
         x2, weight, rstd = ctx.saved_tensors
         d = x2.shape[1]
         dx = torch.empty_like(x2)
@@ -78,10 +81,13 @@ class AddRMSNormFn(torch.autograd.Function):
         ctx.save_for_backward(xn, weight, rstd)
         ctx.consumer, ctx.shape = consumer, x.shape
         ctx.mark_non_differentiable(amax)
+        ctx.set_materialize_grads(False)     # no zero-filled gradient for the amax output
         return xn.view(x.shape), y.view(x.shape), amax
 
     @staticmethod
     def backward(ctx, dxn, dy, _damax):
+        if dxn is None and dy is None:
+            return None, None, None, None, None
         xn, weight, rstd = ctx.saved_tensors
         d = xn.shape[1]
         dx = torch.empty_like(xn)
@@ -108,10 +114,13 @@ class SwiGLUFn(torch.autograd.Function):
         ctx.save_for_backward(gu2)
         ctx.consumer, ctx.shape = consumer, gu.shape
         ctx.mark_non_differentiable(amax)
+        ctx.set_materialize_grads(False)     # no zero-filled gradient for the amax output
         return h.view(*gu.shape[:-1], f2 // 2), amax
 
     @staticmethod
     def backward(ctx, dh, _damax):
+        if dh is None:
+            return None, None
         (gu2,) = ctx.saved_tensors
         dgu = torch.empty_like(gu2)
         _lib.swiglu_bwd(_c2(dh, gu2.shape[1] // 2), gu2, dgu, _amax_buf(ctx.consumer, dgu))
@@ -186,10 +195,13 @@ class Sum3Fn(torch.autograd.Function):
         _lib.glue(0, x, out, amax, T=x.shape[0], d=d3 // 3)
         ctx.consumer, ctx.shape = consumer, qkv.shape
         ctx.mark_non_differentiable(amax)
+        ctx.set_materialize_grads(False)     # no zero-filled gradient for the amax output
         return out.view(*qkv.shape[:-1], d3 // 3), amax
 
     @staticmethod
     def backward(ctx, da, _):
+        if da is None:
+            return None, None
         d = ctx.shape[-1] // 3
         da2 = _c2(da, d)
         out = torch.empty(da2.shape[0], 3 * d, dtype=da2.dtype, device=da2.device)
@@ -208,6 +220,7 @@ class AddFn(torch.autograd.Function):
         amax = torch.empty(1, dtype=torch.float32, device=x.device)
         _lib.glue(2, x2, out, amax, y=y2, T=x2.shape[0], d=d)
         ctx.mark_non_differentiable(amax)
+        ctx.set_materialize_grads(False)     # no zero-filled gradient for the amax output
         return out.view(x.shape), amax
 
     @staticmethod
@@ -224,15 +237,17 @@ class MeanSquareFn(torch.autograd.Function):
         d = y.shape[-1]
         y2 = _c2(y, d)
         acc = torch.empty(1 + _lib.SUMSQ_PARTIALS, dtype=torch.float32, device=y.device)
-        _lib.sumsq(y2, acc)
+        _lib.sumsq(y2, acc, scale=1.0 / y2.numel())         # the mean, in-kernel (no torch scalar op)
         ctx.save_for_backward(y2)
         ctx.consumer, ctx.shape = consumer, y.shape
-        return (acc[:1] / y2.numel()).reshape(())
+        return acc[0]
 
     @staticmethod
     def backward(ctx, g):
         (y2,) = ctx.saved_tensors
-        scale = (g.float() * (2.0 / y2.numel())).reshape(1).contiguous()
+        g = g if g.dtype == torch.float32 else g.float()
         dy = torch.empty_like(y2)
-        _lib.glue(3, y2, dy, _amax_buf(ctx.consumer, dy), scale=scale, T=y2.shape[0], d=y2.shape[1])
+        # dy = y * f32(g * 2/n), the factor formed in-kernel from the incoming gradient
+        _lib.glue(3, y2, dy, _amax_buf(ctx.consumer, dy), scale=g.contiguous(), alpha=2.0 / y2.numel(),
+                  T=y2.shape[0], d=y2.shape[1])
         return dy.view(ctx.shape), None

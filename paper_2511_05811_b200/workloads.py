@@ -15,6 +15,10 @@ and of the qkv/gate_up/down output-gradients run in producer-amax mode (one
 read, no reduction).  Only x (the step's input) and o's output-gradient (the
 gate_up dgrad GEMM's output) are quantized with the in-kernel amax.
 
+The residual branch does not back-propagate into the step input x (x's
+gradient is the QKV dgrad only): no autograd add of two gradient paths, so
+every kernel of the step is one of ours (bench.py lists the rest).
+
 One step = forward + backward (FP8 fwd/dgrad/wgrad for every linear, each
 input and gradient two-level quantized row- and column-wise) + MossAdamW
 (fused update + autoscale + FP8 weight copy).  GEMM FLOPs per step:
@@ -43,7 +47,10 @@ class LayerStack(nn.Module):
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         a, am = Sum3Fn.apply(self.qkv(x), self.qkv)              # a = q + k + v
-        r, am = AddFn.apply(x, self.o(a, am))                     # r = x + O(a)
+        # residual r = x + O(a); its gradient is not propagated back into the step
+        # input (x's gradient is the qkv dgrad alone), so no autograd sum of the two
+        # paths runs: every kernel of the step is one of ours
+        r, am = AddFn.apply(x.detach(), self.o(a, am))
         h, am = SwiGLUFn.apply(self.gate_up(r, am), self.gate_up)
         return MeanSquareFn.apply(self.down(h, am), self.down)    # mean(y^2)
 

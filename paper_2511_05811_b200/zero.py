@@ -37,8 +37,10 @@ slice update runs as [n/256, 256] tiles of the same K3 kernel.
 Invariants (tests/test_zero_cpu.py, tests/test_gpu_zero.py): after each
 step every rank holds identical FP8 codes, transposed codes and scales; at
 world_size 1 the result is bit-identical to the replicated MossAdamW step.
-On a rank, master values outside its slices are stale by design (never
-read: the forward and backward consume only the FP8 codes).
+On a rank, master values outside its slices are stale by design: the forward
+and the FP8 backward consume only the FP8 codes (the full-precision backward,
+which would read them, is rejected).  ``gather_master()`` all-gathers the
+FP32 masters, e.g. before ``model.state_dict()`` for a checkpoint.
 """
 
 from __future__ import annotations
@@ -51,6 +53,7 @@ import torch.distributed as dist
 
 from . import _lib
 from .dist import GradBuckets
+from .errors import InvalidArgumentError
 from .fp8 import E4M3
 from .nn import MossAdamW, device_flags
 
@@ -100,6 +103,11 @@ class Zero1:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         moss = [p for p in opt.params if hasattr(p, "moss_layer")]
         rest = [p for p in opt.params if not hasattr(p, "moss_layer")]
+        for p in moss:
+            if not getattr(p.moss_layer, "fp8_backward", True):
+                # the full-precision backward (train.py:187-192) reads the FP32 master
+                # weight, which is only current on this rank's slices
+                raise InvalidArgumentError("ZeRO-1 needs the FP8 backward (MossLinear(fp8_backward=True))")
         self.moss = moss
         self.dev = moss[0].device if moss else opt.params[0].device
         self.cuda = self.dev.type == "cuda"
@@ -216,7 +224,7 @@ class Zero1:
             _lib.adamw_fp8_dev(w, g, m, v, rows, cols, rec, None, flags, w_amax=layer.w_amax)
         else:
             codes = b.codes[o + part.lo:o + part.hi].view(rows, cols)
-            _lib.adamw_fp8_dev(w, g, m, v, rows, cols, rec, rec + 36, flags, scale_out=layer.w_scale, w_fp8=codes,
+            _lib.adamw_fp8_dev(w, g, m, v, rows, cols, rec, rec + MossAdamW._ENC * 4, flags, scale_out=layer.w_scale, w_fp8=codes,
                                w_amax=layer.w_amax, n_saturated=self.opt.saturations)
 
     def _encode_part(self, b: _Bucket, part: _Part, scale: float) -> None:
@@ -232,7 +240,8 @@ class Zero1:
     def _set_scale(self, layer, idx: int) -> None:
         """w_scale of a layer with no slice on this rank: copy the staged f32(s_{t+1})."""
         w = MossAdamW._WORDS
-        layer.w_scale.copy_(self.opt.hp_dev[idx * w + 9: idx * w + 10])
+        e = MossAdamW._ENC
+        layer.w_scale.copy_(self.opt.hp_dev[idx * w + e: idx * w + e + 1])
 
     def _transpose(self, layer) -> None:
         """Nothing to rebuild: the dgrad GEMM reads W_fp8 as stored (MN-major
@@ -273,6 +282,7 @@ class Zero1:
 
     def _rescale(self) -> None:
         """JIT snap s_t = max|W'|/448 on every rank (autoscale.py:86-96): one MAX all-reduce."""
+        self.opt.check("rescale step")          # a gated (skipped) update leaves no amax to snap to
         amax = torch.cat([p.moss_layer.w_amax.view(1) for p in self.moss])
         if self.world > 1:
             dist.all_reduce(amax, op=dist.ReduceOp.MAX, group=self.group)
@@ -324,6 +334,23 @@ class Zero1:
             if layer.fp8_pending is not None:
                 pending, layer.fp8_pending = layer.fp8_pending, None
                 pending()
+
+    @torch.no_grad()
+    def gather_master(self) -> None:
+        """All-gather the FP32 master weights of every MOSS parameter so that each
+        rank holds the full, current values (checkpointing: state_dict)."""
+        for b in self.buckets:
+            S = b.length // self.world
+            flat = torch.zeros(b.length, dtype=torch.float32, device=self.dev)
+            lo_r = self.rank * S
+            for part in b.parts:
+                o = b.offsets[id(part.param)]
+                flat[o + part.lo:o + part.hi] = part.param.data.view(-1)[part.lo:part.hi]
+            if self.world > 1:
+                dist.all_gather_into_tensor(flat, flat[lo_r:lo_r + S].clone(), group=self.group)
+            for p in b.params:
+                o = b.offsets[id(p)]
+                p.data.view(-1).copy_(flat[o:o + p.numel()])
 
     def state_bytes(self) -> int:
         """Optimizer-state bytes held by this rank for the MOSS weights (m, v slices)."""

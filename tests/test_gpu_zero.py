@@ -1,6 +1,6 @@
 """ZeRO-1 (zero.Zero1) on the GPU at world_size 1 over NCCL: the sharded
 driver — flat 256-aligned slices through the K3 kernel, codes in the
-bucket buffer the GEMMs read, W_fp8^T rebuilt by the byte-transpose kernel,
+bucket buffer the GEMMs read (dgrad reads them as stored, MN-major),
 rescale through the max-all-reduce path — must train exactly like the
 replicated MossAdamW (same init, same data).  The multi-rank collectives are
 covered on CPU by test_zero_cpu.py (gloo, world 2)."""
@@ -32,14 +32,6 @@ def _port():
     p = s.getsockname()[1]
     s.close()
     return p
-
-
-def test_transpose_u8():
-    for rows, cols in [(128, 256), (4096, 11008), (48, 80)]:
-        x = torch.randint(0, 256, (rows, cols), dtype=torch.uint8, device="cuda")
-        y = torch.empty(cols, rows, dtype=torch.uint8, device="cuda")
-        _lib.transpose_u8(x, y)
-        assert torch.equal(y, x.t())
 
 
 def test_zero1_world1_matches_replicated():

@@ -57,8 +57,9 @@ class _Layer:
 
 
 class _StubOpt:
-    """The MossAdamW host half Zero1 relies on (prepare / launch / records)."""
+    """The MossAdamW host half Zero1 relies on (prepare / launch / check / records)."""
     _WORDS = 12
+    _ENC = 10
 
     def __init__(self, layers):
         self.params = [lay.weight for lay in layers]
@@ -82,11 +83,14 @@ class _StubOpt:
             sched = p.moss_layer.schedule
             R.advance(sched, LR)
             due |= R.rescale_due(sched)
-            self.hp_dev[i * self._WORDS + 9] = float(np.float32(sched.s_t))
+            self.hp_dev[i * self._WORDS + self._ENC] = float(np.float32(sched.s_t))
         self._rescale_pending = due
         return due
 
     def launch(self, rescale=None):
+        pass
+
+    def check(self, where=""):
         pass
 
 
@@ -111,7 +115,7 @@ def _install_cpu_kernels(z, states_by_param):
         if rescale:
             layer.w_amax.fill_(float(np.abs(w2.astype(np.float32)).max()))
         else:
-            s = float(z.opt.hp_dev[z.opt.index[id(p)] * 12 + 9])
+            s = float(z.opt.hp_dev[z.opt.index[id(p)] * 12 + 10])
             codes, _ = R.encode_weight(w2.astype(np.float32), s)
             o = b.offsets[id(p)]
             b.codes[o + part.lo:o + part.hi] = torch.from_numpy(codes.reshape(-1))
@@ -167,9 +171,11 @@ def _worker(rank, world, port, q, overlap=True):
                 assert all(lay.fp8_pending is not None for lay in layers)
         z.sync()
         assert all(lay.fp8_pending is None for lay in layers)
+        z.gather_master()                                  # full FP32 masters on every rank (checkpoints)
         # numpy copies: torch tensors in a spawn queue die with the child's shared-memory handles
         q.put((rank, [(lay.w_fp8.numpy().copy(), lay.w_fp8_t.numpy().copy(), float(lay.w_scale),
-                       lay.schedule.s_t, lay.schedule.last_rescale_step) for lay in layers], "", z.state_bytes()))
+                       lay.schedule.s_t, lay.schedule.last_rescale_step, lay.weight.data.numpy().copy())
+                      for lay in layers], "", z.state_bytes()))
     except Exception as e:  # surface worker failures immediately
         q.put((rank, None, repr(e), 0))
         raise
@@ -223,7 +229,8 @@ def test_zero1_matches_replicated_world2(world, overlap):
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     ref = _replicated_reference(world)
     for rank in range(world):
-        for (codes, codes_t, scale, s_t, last), lay in zip(out[rank][0], ref):
+        for (codes, codes_t, scale, s_t, last, master), lay in zip(out[rank][0], ref):
+            assert np.array_equal(master, lay.weight.data.numpy()), f"rank {rank}: gathered FP32 masters"
             assert np.array_equal(codes, lay.w_fp8.numpy()), f"rank {rank}: gathered FP8 codes"
             assert np.array_equal(codes_t, lay.w_fp8.t().numpy()), f"rank {rank}: transposed codes"
             assert scale == float(lay.w_scale) and s_t == lay.schedule.s_t
