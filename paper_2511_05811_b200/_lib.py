@@ -141,7 +141,9 @@ class FlagWord:
     because an error bit was already set (0xFFFFFFFF = none)."""
 
     def __init__(self, device=None):
-        self.t = torch.tensor([0, -1], dtype=torch.int32, device=device or "cuda")
+        # no host->device copy: a flag word may be created during CUDA-graph capture
+        self.t = torch.zeros(2, dtype=torch.int32, device=device or "cuda")
+        self.t[1:].fill_(-1)
         self._init = self.t.clone()
 
     @property
@@ -185,11 +187,13 @@ class Instrument:
     def __init__(self):
         self.active = False
         self.timing = False
+        self.external = False     # events captured into a CUDA graph (timeline of replays); records only while capturing
         self.launches = 0
         self.records: list[tuple[str, float, torch.cuda.Event, torch.cuda.Event]] = []
 
-    def start(self, timing: bool = True) -> None:
+    def start(self, timing: bool = True, external: bool = False) -> None:
         self.active, self.timing, self.launches, self.records = True, timing, 0, []
+        self.external = external
 
     def stop(self) -> None:
         self.active = False
@@ -214,8 +218,8 @@ class _Span:
         self.kind, self.work, self.s = kind, work, None
         if INSTR.active:
             INSTR.launches += kernels
-            if INSTR.timing:
-                self.s = torch.cuda.Event(enable_timing=True)
+            if INSTR.timing and (not INSTR.external or torch.cuda.is_current_stream_capturing()):
+                self.s = torch.cuda.Event(enable_timing=True, external=INSTR.external)
                 self.s.record()
 
     def __enter__(self):
@@ -223,7 +227,7 @@ class _Span:
 
     def __exit__(self, *exc):
         if self.s is not None and exc[0] is None:
-            e = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True, external=INSTR.external)
             e.record()
             INSTR.records.append((self.kind, self.work, self.s, e))
         return False
