@@ -117,11 +117,15 @@ int moss_encode_scaled(const void* x, int dtype, int64_t rows, int64_t cols, con
  * layout (SFB == NULL means unit scales: the per-tensor weight side,
  * PAPER.md:103).  D is [M, N] row-major (ldd elements), bf16 or f32;
  * accumulate != 0 adds into D (f32 only).  K % 128 == 0, M, N >= 1.
+ * d_amax (nullable): receives max|D| of the stored values as f32 (zeroed by the
+ * call; the amax epilogue for the quantizer that consumes D, quantize.py:149-155
+ * — not with accumulate, and D contiguous (ldd == N)); flags receives
+ * MOSS_FLAG_NONFINITE from the separate amax pass of the 1-CTA fallback.
  * The reference returns (out_features, tokens): call with A = weights,
  * B = activations for that orientation, or A = activations for torch's. */
 int moss_gemm_mxf8(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB,
                    const float* sA, const float* sB, void* D, int d_dtype, int64_t ldd,
-                   int64_t M, int64_t N, int64_t K, int accumulate, void* stream);
+                   int64_t M, int64_t N, int64_t K, int accumulate, float* d_amax, uint32_t* flags, void* stream);
 
 /* K3 hyper-parameters of one AdamW step (optim.py:52-62, 78-106). */
 typedef struct {
@@ -146,9 +150,11 @@ int moss_check_finite(const void* x, int dtype, int64_t n, uint32_t bit, uint32_
  * B scales: the dgrad product dX = dY W reads the per-tensor E4M3 weight codes
  * W [out = K, in = N] directly (MN-major tcgen05 operand) — no transposed copy
  * of W is kept (replaces the W^T operand of gemm.py:115-129 in the backward).
- * M % 256, N % 256, K % 128. */
+ * M % 256, N % 256, K % 128.  d_amax (nullable): max|D| as for moss_gemm_mxf8 — the
+ * dgrad output is the next layer's output-gradient, quantized next. */
 int moss_gemm_mxf8_bkn(const uint8_t* A, const uint8_t* SFA, const uint8_t* B_kn, const float* sA, const float* sB,
-                       void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, void* stream);
+                       void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, float* d_amax,
+                       void* stream);
 
 /* K3: fused AdamW + automatic scaling + FP8 weight copy
  * (adamw_step optim.py:78-106, then _quantize_weight train.py:113-118 at the

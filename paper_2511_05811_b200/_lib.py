@@ -46,13 +46,13 @@ _SIGS = {
     "moss_rope_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
     "moss_cross_entropy_fwd": (_I, [_P, _P, _P, _P, _I64, _I64, _P]),
     "moss_glue": (_I, [_I, _P, _P, _P, _F, _P, _P, _I64, _I64, _P]),
-    "moss_gemm_mxf8_bkn": (_I, [_P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _P]),
+    "moss_gemm_mxf8_bkn": (_I, [_P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _P, _P]),
     "moss_sumsq": (_I, [_P, _I64, _F, _P, _P, _P]),
     "moss_cross_entropy_bwd": (_I, [_P, _P, _P, _P, _P, _I64, _I64, _P]),
     "moss_quant_per_group": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P, _P]),
     "moss_gemm_pergroup": (_I, [_P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _P]),
     "moss_encode_scaled": (_I, [_P, _I, _I64, _I64, _P, _F, _I, _P, _P, _P, _P, _P, _P]),
-    "moss_gemm_mxf8": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _I, _P]),
+    "moss_gemm_mxf8": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _I, _P, _P, _P]),
     "moss_check_finite": (_I, [_P, _I, _I64, ctypes.c_uint32, _P, _P]),
     "moss_adamw_fp8": (_I, [_P, _P, _I, _P, _P, _I64, _I64, ctypes.POINTER(AdamParams), _F, _P, _P, _P,
                             _P, _P, _P]),
@@ -277,23 +277,27 @@ def encode_scaled(x2d: torch.Tensor, flags: FlagWord, *, scale_t=None, scale_hos
               "moss_encode_scaled")
 
 
-def gemm(a, sfa, b, sfb, s_a, s_b, d, *, accumulate: bool = False) -> None:
+def gemm(a, sfa, b, sfb, s_a, s_b, d, *, accumulate: bool = False, amax=None, flags: "FlagWord | None" = None) -> None:
+    """``amax`` (device f32 [1], optional): receives max|D| (the amax epilogue)."""
     m, k = a.shape
     n = b.shape[0]
+    if amax is not None and flags is None:
+        flags = FlagWord(d.device)
     with _Span("gemm", 2.0 * m * n * k):
         check(lib().moss_gemm_mxf8(a.data_ptr(), sfa.data_ptr(), b.data_ptr(), ptr(sfb), s_a.data_ptr(),
                                    s_b.data_ptr(), d.data_ptr(), dtype_code(d), d.stride(0), m, n, k,
-                                   int(accumulate), stream()),
+                                   int(accumulate), ptr(amax), ptr(flags), stream()),
               "moss_gemm_mxf8")
 
 
-def gemm_bkn(a, sfa, b_kn, s_a, s_b, d) -> None:
-    """D = A B with B = b_kn [K, N] row-major (the weight as stored), unit B scales."""
+def gemm_bkn(a, sfa, b_kn, s_a, s_b, d, *, amax=None) -> None:
+    """D = A B with B = b_kn [K, N] row-major (the weight as stored), unit B scales;
+    ``amax`` (device f32 [1], optional) receives max|D|."""
     m, k = a.shape
     n = b_kn.shape[1]
     with _Span("gemm", 2.0 * m * n * k):
         check(lib().moss_gemm_mxf8_bkn(a.data_ptr(), sfa.data_ptr(), b_kn.data_ptr(), s_a.data_ptr(), s_b.data_ptr(),
-                                       d.data_ptr(), dtype_code(d), d.stride(0), m, n, k, stream()),
+                                       d.data_ptr(), dtype_code(d), d.stride(0), m, n, k, ptr(amax), stream()),
               "moss_gemm_mxf8_bkn")
 
 

@@ -18,9 +18,10 @@ int launch_encode_scaled(const void* x, int dtype, int64_t rows, int64_t cols, c
                          uint32_t* flags, cudaStream_t st);
 int launch_gemm(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
                 const float* sB, void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
-                cudaStream_t st);
+                float* d_amax, uint32_t* flags, cudaStream_t st);
 int launch_gemm2_bkn(const uint8_t* A, const uint8_t* SFA, const uint8_t* B_kn, const float* sA, const float* sB,
-                     void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, cudaStream_t st);
+                     void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, float* d_amax,
+                     cudaStream_t st);
 int launch_adamw(float* w, const void* g, int g_dtype, float* m, float* v, int64_t rows, int64_t cols,
                  const moss_adam_params& p, float enc_scale, const moss_adam_params* p_dev, const float* enc_dev,
                  float* scale_out, uint8_t* w_fp8, uint8_t* w_fp8_t, float* w_amax, uint32_t* nsat,
@@ -126,28 +127,31 @@ int moss_encode_scaled(const void* x, int dtype, int64_t rows, int64_t cols, con
 
 int moss_gemm_mxf8(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
                    const float* sB, void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
-                   void* stream) {
+                   float* d_amax, uint32_t* flags, void* stream) {
     if (M <= 0 || N <= 0 || K <= 0) return MOSS_ERR_SHAPE;
     if (K % 128 || M % 128 || N % 128) return MOSS_ERR_SHAPE;
     if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return MOSS_ERR_SHAPE;
     if (!A || !B || !SFA || !sA || !sB || !D || !dtype_ok(d_dtype)) return MOSS_ERR_ARGUMENT;
     if (ldd < N) return MOSS_ERR_SHAPE;
     if (accumulate && d_dtype != MOSS_F32) return MOSS_ERR_ARGUMENT;
+    if (d_amax && (accumulate || ldd != N || !flags)) return MOSS_ERR_ARGUMENT;
     if (!aligned(A, 16) || !aligned(B, 16) || !aligned(SFA, 16) || (SFB && !aligned(SFB, 16)) || !aligned(D, 16) ||
         ldd % 8)
         return MOSS_ERR_ALIGN;
-    return moss::launch_gemm(A, SFA, B, SFB, sA, sB, D, d_dtype, ldd, M, N, K, accumulate, (cudaStream_t)stream);
+    return moss::launch_gemm(A, SFA, B, SFB, sA, sB, D, d_dtype, ldd, M, N, K, accumulate, d_amax, flags,
+                             (cudaStream_t)stream);
 }
 
 int moss_gemm_mxf8_bkn(const uint8_t* A, const uint8_t* SFA, const uint8_t* B_kn, const float* sA, const float* sB,
-                       void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, void* stream) {
+                       void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, float* d_amax,
+                       void* stream) {
     if (M <= 0 || N <= 0 || K <= 0) return MOSS_ERR_SHAPE;
     if (K % 128 || M % 256 || N % 256) return MOSS_ERR_SHAPE;
     if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return MOSS_ERR_SHAPE;
     if (!A || !B_kn || !SFA || !sA || !sB || !D || !dtype_ok(d_dtype)) return MOSS_ERR_ARGUMENT;
     if (ldd < N) return MOSS_ERR_SHAPE;
     if (!aligned(A, 16) || !aligned(B_kn, 16) || !aligned(SFA, 16) || !aligned(D, 16) || ldd % 8) return MOSS_ERR_ALIGN;
-    return moss::launch_gemm2_bkn(A, SFA, B_kn, sA, sB, D, d_dtype, ldd, M, N, K, (cudaStream_t)stream);
+    return moss::launch_gemm2_bkn(A, SFA, B_kn, sA, sB, D, d_dtype, ldd, M, N, K, d_amax, (cudaStream_t)stream);
 }
 
 int moss_adamw_fp8(float* w, const void* g, int g_dtype, float* m, float* v, int64_t rows, int64_t cols,

@@ -256,7 +256,8 @@ static int launch_gemm_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B,
 
 int launch_gemm2(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
                  const float* sB, void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
-                 cudaStream_t st);
+                 float* d_amax, cudaStream_t st);
+int launch_amax(const void* x, int dtype, int64_t n, float* amax, uint32_t* flags, cudaStream_t st);
 
 static int gemm_variant() {
     static int v = -1;
@@ -269,18 +270,22 @@ static int gemm_variant() {
 
 int launch_gemm(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
                 const float* sB, void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
-                cudaStream_t st) {
+                float* d_amax, uint32_t* flags, cudaStream_t st) {
     if (gemm_variant() == 2) {
-        const int r = launch_gemm2(A, SFA, B, SFB, sA, sB, D, d_dtype, ldd, M, N, K, accumulate, st);
+        const int r = launch_gemm2(A, SFA, B, SFB, sA, sB, D, d_dtype, ldd, M, N, K, accumulate, d_amax, st);
         if (r >= 0) return r;
     }
     const bool bn256 = (N % 256) == 0;
-    if (d_dtype == MOSS_BF16) {
-        return bn256 ? launch_gemm_t<256, 4, true>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
-                     : launch_gemm_t<128, 6, true>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st);
-    }
-    return bn256 ? launch_gemm_t<256, 4, false>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st)
-                 : launch_gemm_t<128, 6, false>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
+    int r;
+    if (d_dtype == MOSS_BF16)
+        r = bn256 ? launch_gemm_t<256, 4, true>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
+                  : launch_gemm_t<128, 6, true>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st);
+    else
+        r = bn256 ? launch_gemm_t<256, 4, false>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st)
+                  : launch_gemm_t<128, 6, false>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
+    // the 1-CTA kernel has no amax epilogue: a separate pass over D (contiguous D only, checked by the caller)
+    if (r == MOSS_OK && d_amax) r = launch_amax(D, d_dtype, M * N, d_amax, flags, st);
+    return r;
 }
 
 }  // namespace moss

@@ -120,7 +120,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                           const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
                           const __grid_constant__ CUtensorMap tmD, void* __restrict__ D, int64_t ldd,
                           const float* __restrict__ sA, const float* __restrict__ sB, int M, int N, int K,
-                          int unit_b, int accumulate, int raster) {
+                          int unit_b, int accumulate, int raster, uint32_t* __restrict__ d_amax) {
     using L = G2Layout<STAGES, TMA_EPI, EPI_WARPS, BN>;
     constexpr int ACC = L::ACC;
     constexpr int COLS = BN / (EPI_WARPS / 4);      // accumulator columns per epilogue warp
@@ -300,6 +300,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
         uint8_t* stg = s_stg + ew * L::STG_BYTES;
         const uint32_t stg_s = smem_u32(stg);
         const float alpha = __fmul_rn(*sA, *sB);
+        // max |D| of the stored values (bf16: both halves of each packed word; f32: the
+        // magnitude bits) for the quantizer that consumes D (producer-fused amax)
+        uint32_t am = 0;
         uint32_t acc_phase = 0;
         int it_ = 0;
         for (int tile = pair; tile < num_tiles; tile += npairs, ++it_) {
@@ -342,6 +345,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                         o.y = pack_bf16(__uint_as_float(r[8 * c + 2]) * alpha, __uint_as_float(r[8 * c + 3]) * alpha);
                         o.z = pack_bf16(__uint_as_float(r[8 * c + 4]) * alpha, __uint_as_float(r[8 * c + 5]) * alpha);
                         o.w = pack_bf16(__uint_as_float(r[8 * c + 6]) * alpha, __uint_as_float(r[8 * c + 7]) * alpha);
+                        am = __vmaxu2(__vmaxu2(am, o.x & 0x7FFF7FFFu), o.y & 0x7FFF7FFFu);
+                        am = __vmaxu2(__vmaxu2(am, o.z & 0x7FFF7FFFu), o.w & 0x7FFF7FFFu);
                         dst[c] = o;
                     }
                 } else {
@@ -354,6 +359,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                             const float4 p = dst[c];
                             o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
                         }
+                        am = max(max(am, __float_as_uint(o.x) & 0x7FFFFFFFu), __float_as_uint(o.y) & 0x7FFFFFFFu);
+                        am = max(max(am, __float_as_uint(o.z) & 0x7FFFFFFFu), __float_as_uint(o.w) & 0x7FFFFFFFu);
                         dst[c] = o;
                     }
                 }
@@ -374,12 +381,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                             o.y = pack_bf16(__uint_as_float(q[2]) * alpha, __uint_as_float(q[3]) * alpha);
                             o.z = pack_bf16(__uint_as_float(q[4]) * alpha, __uint_as_float(q[5]) * alpha);
                             o.w = pack_bf16(__uint_as_float(q[6]) * alpha, __uint_as_float(q[7]) * alpha);
+                            am = __vmaxu2(__vmaxu2(am, o.x & 0x7FFF7FFFu), o.y & 0x7FFF7FFFu);
+                            am = __vmaxu2(__vmaxu2(am, o.z & 0x7FFF7FFFu), o.w & 0x7FFF7FFFu);
                         } else {
                             const uint32_t* q = &r[16 * h + 4 * c];
                             o.x = __float_as_uint(__uint_as_float(q[0]) * alpha);
                             o.y = __float_as_uint(__uint_as_float(q[1]) * alpha);
                             o.z = __float_as_uint(__uint_as_float(q[2]) * alpha);
                             o.w = __float_as_uint(__uint_as_float(q[3]) * alpha);
+                            am = max(max(am, o.x & 0x7FFFFFFFu), max(o.y & 0x7FFFFFFFu, o.z & 0x7FFFFFFFu));
+                            am = max(am, o.w & 0x7FFFFFFFu);     // (d_amax is refused with accumulate)
                         }
                         sts128(stg_s + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4), o.x, o.y, o.z, o.w);
                     }
@@ -397,6 +408,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
             }
         }
         if (TMA_EPI && lane == 0) bulk_wait0();
+        if (d_amax) {
+            // as f32 bits: |x| orders like its bits; NaN/Inf land at >= 0x7F800000 (flagged by the quantizer)
+            uint32_t v = OUT_BF16 ? (max(am & 0xFFFFu, am >> 16) << 16) : am;
+            v = __reduce_max_sync(0xFFFFFFFFu, v);
+            if (lane == 0 && v) atomicMax(d_amax, v);
+        }
     }
     tc_fence_before();
     cluster_sync_all();
@@ -435,7 +452,7 @@ static int g2_raster(int64_t m_pairs, int64_t n_tiles, int BN, int64_t K) {
 template <bool OUT_BF16, int STAGES, bool TMA_EPI, int EPI_WARPS, int BN = 256, bool B_MN = false>
 static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
                           const float* sB, void* D, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
-                          cudaStream_t st) {
+                          float* d_amax, cudaStream_t st) {
     using L = G2Layout<STAGES, TMA_EPI, EPI_WARPS, BN>;
     auto kern = gemm_mxf8_2cta_kernel<OUT_BF16, STAGES, TMA_EPI, EPI_WARPS, BN, B_MN>;
     static bool attr_set[kMaxDevices] = {};
@@ -469,8 +486,10 @@ static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B
     const int64_t tiles = (M / (2 * G2_BM)) * (N / BN);
     const int pairs = (int)std::min<int64_t>(tiles, sm_count() / 2);
     const int raster = g2_raster(M / (2 * G2_BM), N / BN, BN, K);
+    if (d_amax && cudaMemsetAsync(d_amax, 0, sizeof(float), st) != cudaSuccess) return MOSS_ERR_CUDA;
     kern<<<2 * pairs, (4 + EPI_WARPS) * 32, L::SMEM, st>>>(ta, tb, tsa, tsb, td, D, ldd, sA, sB, (int)M, (int)N, (int)K,
-                                                 SFB == nullptr, accumulate, raster);
+                                                 SFB == nullptr, accumulate, raster,
+                                                 reinterpret_cast<uint32_t*>(d_amax));
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 
@@ -490,26 +509,27 @@ static int gemm2_mode() {
 // returns -1 when the shape is not covered by the pair kernel
 int launch_gemm2(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
                  const float* sB, void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
-                 cudaStream_t st) {
+                 float* d_amax, cudaStream_t st) {
     if (M % (2 * G2_BM) || N % 128 || K % G2_BK) return -1;
     if ((reinterpret_cast<uintptr_t>(D) % 16) || (ldd * (d_dtype == MOSS_BF16 ? 2 : 4)) % 16) return -1;
     const bool bf = d_dtype == MOSS_BF16;
     const bool n128 = gemm2_mode() == 3 || N % G2_BN != 0;
     if (n128)
-        return bf ? launch_gemm2_t<true, 8, true, 8, 128>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
-                  : launch_gemm2_t<false, 8, true, 8, 128>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
-    return bf ? launch_gemm2_t<true, 6, true, 8>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, st)
-              : launch_gemm2_t<false, 6, true, 8>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, st);
+        return bf ? launch_gemm2_t<true, 8, true, 8, 128>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, d_amax, st)
+                  : launch_gemm2_t<false, 8, true, 8, 128>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, d_amax, st);
+    return bf ? launch_gemm2_t<true, 6, true, 8>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, 0, d_amax, st)
+              : launch_gemm2_t<false, 6, true, 8>(A, SFA, B, SFB, sA, sB, D, ldd, M, N, K, accumulate, d_amax, st);
 }
 
 // dgrad with the weight as stored: B = W [K, N] row-major, per-tensor (unit SF)
 int launch_gemm2_bkn(const uint8_t* A, const uint8_t* SFA, const uint8_t* B_kn, const float* sA, const float* sB,
-                     void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, cudaStream_t st) {
+                     void* D, int d_dtype, int64_t ldd, int64_t M, int64_t N, int64_t K, float* d_amax,
+                     cudaStream_t st) {
     if (M % (2 * G2_BM) || N % G2_BN || K % G2_BK) return MOSS_ERR_SHAPE;
     if ((reinterpret_cast<uintptr_t>(D) % 16) || (ldd * (d_dtype == MOSS_BF16 ? 2 : 4)) % 16) return MOSS_ERR_ALIGN;
     return d_dtype == MOSS_BF16
-               ? launch_gemm2_t<true, 6, true, 8, 256, true>(A, SFA, B_kn, nullptr, sA, sB, D, ldd, M, N, K, 0, st)
-               : launch_gemm2_t<false, 6, true, 8, 256, true>(A, SFA, B_kn, nullptr, sA, sB, D, ldd, M, N, K, 0, st);
+               ? launch_gemm2_t<true, 6, true, 8, 256, true>(A, SFA, B_kn, nullptr, sA, sB, D, ldd, M, N, K, 0, d_amax, st)
+               : launch_gemm2_t<false, 6, true, 8, 256, true>(A, SFA, B_kn, nullptr, sA, sB, D, ldd, M, N, K, 0, d_amax, st);
 }
 
 }  // namespace moss

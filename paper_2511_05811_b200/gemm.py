@@ -126,12 +126,14 @@ def _pad_codes(codes: torch.Tensor, rows: int, cols: int) -> torch.Tensor:
 
 def mx_gemm(a_codes: torch.Tensor, a_sf: torch.Tensor | None, s_a: torch.Tensor, b_codes: torch.Tensor,
             b_sf: torch.Tensor | None, s_b: torch.Tensor, *, out: torch.Tensor | None = None,
-            out_dtype: torch.dtype = torch.bfloat16, accumulate: bool = False) -> torch.Tensor:
+            out_dtype: torch.dtype = torch.bfloat16, accumulate: bool = False,
+            amax_out: torch.Tensor | None = None) -> torch.Tensor:
     """D[M, N] = (A . SFA)(B . SFB)^T * s_a * s_b on tcgen05 (one launch).
 
     a_codes [M, K], b_codes [N, K] uint8 E4M3; a_sf / b_sf block-scale buffers
     (None = unit scales, i.e. a per-tensor operand); s_a, s_b 1-element f32
-    device tensors.  Non-multiple-of-128 shapes are zero padded.
+    device tensors.  Non-multiple-of-128 shapes are zero padded.  ``amax_out``
+    (device f32 [1]) receives max|D| from the epilogue (not with accumulate).
     """
     m, k = a_codes.shape
     n, kb = b_codes.shape
@@ -155,7 +157,9 @@ def mx_gemm(a_codes: torch.Tensor, a_sf: torch.Tensor | None, s_a: torch.Tensor,
             d[:m, :n] = out
         else:
             d = torch.empty((mp, np_), dtype=out.dtype if out is not None else out_dtype, device=dev)
-    _lib.gemm(a, a_sf, b, b_sf, s_a, s_b, d, accumulate=accumulate)
+    if amax_out is not None and (accumulate or not d.is_contiguous()):
+        raise InvalidArgumentError("the amax epilogue needs a fresh, contiguous output")
+    _lib.gemm(a, a_sf, b, b_sf, s_a, s_b, d, accumulate=accumulate, amax=amax_out)
     if d is out:
         return out
     if out is not None:
@@ -165,19 +169,23 @@ def mx_gemm(a_codes: torch.Tensor, a_sf: torch.Tensor | None, s_a: torch.Tensor,
 
 
 def mx_gemm_bkn(a_codes: torch.Tensor, a_sf: torch.Tensor, s_a: torch.Tensor, w_codes: torch.Tensor,
-                s_w: torch.Tensor, *, out_dtype: torch.dtype = torch.bfloat16) -> torch.Tensor:
+                s_w: torch.Tensor, *, out_dtype: torch.dtype = torch.bfloat16, out: torch.Tensor | None = None,
+                amax_out: torch.Tensor | None = None) -> torch.Tensor:
     """D[M, N] = (A . SFA) W * s_a * s_w with W = w_codes [K, N] as stored (per-tensor
     E4M3, unit scales): the dgrad product dX = dY W without a transposed copy of W
     (MN-major tcgen05 B operand).  Shapes off the kernel's grid (M % 256, N % 256,
-    K % 128) go through ``mx_gemm`` with W^T materialised."""
+    K % 128) go through ``mx_gemm`` with W^T materialised.  ``amax_out`` (device
+    f32 [1]) receives max|D| (the amax epilogue: D is the next output-gradient
+    to be quantized)."""
     m, k = a_codes.shape
     kw, n = w_codes.shape
     if k != kw:
         raise InvalidShapeError(f"K mismatch: {k} vs {kw}")
     if m % 256 or n % 256 or k % 128 or not w_codes.is_contiguous() or not a_codes.is_contiguous():
-        return mx_gemm(a_codes, a_sf, s_a, w_codes.t().contiguous(), None, s_w, out_dtype=out_dtype)
-    d = torch.empty((m, n), dtype=out_dtype, device=a_codes.device)
-    _lib.gemm_bkn(a_codes, a_sf, w_codes, s_a, s_w, d)
+        return mx_gemm(a_codes, a_sf, s_a, w_codes.t().contiguous(), None, s_w, out_dtype=out_dtype, out=out,
+                       amax_out=amax_out)
+    d = torch.empty((m, n), dtype=out_dtype, device=a_codes.device) if out is None else out
+    _lib.gemm_bkn(a_codes, a_sf, w_codes, s_a, s_w, d, amax=amax_out)
     return d
 
 

@@ -77,9 +77,12 @@ class MossLinearFunction(torch.autograd.Function):
     # bucket view), with no extra pass over the gradient.
     # ``amax`` (optional, device f32 [1]) is max|x| computed by the kernel that
     # produced x (producer-fused amax): the quantizer then skips its reduction.
+    # ``dx_consumer`` (optional MossLinear): the layer that quantizes this layer's
+    # dX as ITS output-gradient (e.g. through a residual add) — the dgrad GEMM then
+    # writes max|dX| for it (the amax epilogue) and that quantizer skips its reduction.
     @staticmethod
     def forward(ctx, x: torch.Tensor, weight: torch.Tensor, layer: "MossLinear",
-                amax: torch.Tensor | None = None) -> torch.Tensor:
+                amax: torch.Tensor | None = None, dx_consumer: "MossLinear | None" = None) -> torch.Tensor:
         k = x.shape[-1]
         n = layer.out_features
         x2d = _aligned_2d(x, k)
@@ -91,6 +94,7 @@ class MossLinearFunction(torch.autograd.Function):
         op = quantize_mx2(x2d, row=True, col=need_w and fp8_bwd, flags=flags, amax=amax)
         y = mx_gemm(op.codes, op.sf, op.g, layer.w_fp8, None, layer.w_scale, out_dtype=torch.bfloat16)
         ctx.layer = layer
+        ctx.dx_consumer = dx_consumer
         ctx.fp8_bwd = fp8_bwd
         if not fp8_bwd:
             # reference semantics (train.py:187-192): backward in full precision at the
@@ -115,7 +119,9 @@ class MossLinearFunction(torch.autograd.Function):
         opd = quantize_mx2(dy2d, row=need_x, col=ctx.need_w, flags=flags, amax=layer.take_dy_amax(dy2d))
         dx = None
         if need_x:
-            dx = mx_gemm_bkn(opd.codes, opd.sf, opd.g, layer.w_fp8, layer.w_scale)   # dY W, W as stored
+            dx = torch.empty((dy2d.shape[0], layer.in_features), dtype=torch.bfloat16, device=dy.device)
+            am = ctx.dx_consumer.offer_dy_amax(dx) if ctx.dx_consumer is not None else None
+            mx_gemm_bkn(opd.codes, opd.sf, opd.g, layer.w_fp8, layer.w_scale, out=dx, amax_out=am)   # dY W, W as stored
             dx = dx.view(ctx.x_shape)
             if dx.dtype != ctx.x_dtype:
                 dx = dx.to(ctx.x_dtype)
@@ -132,7 +138,7 @@ class MossLinearFunction(torch.autograd.Function):
             hook = getattr(w, "grad_ready_hook", None)
             if hook is not None:
                 hook(w)
-        return dx, None, None, None
+        return dx, None, None, None, None
 
     @staticmethod
     def _backward_fp(ctx, dy, layer, need_x):
@@ -155,7 +161,7 @@ class MossLinearFunction(torch.autograd.Function):
             if hook is not None:
                 hook(w)
         layer.take_dy_amax(dy2d)
-        return dx, None, None, None
+        return dx, None, None, None, None
 
 
 class MossLinear(nn.Module):
@@ -235,13 +241,16 @@ class MossLinear(nn.Module):
         self.w_scale.fill_(s)
         _lib.encode_scaled(self.weight.detach(), device_flags(self.weight.device), scale_host=s, codes=self.w_fp8)
 
-    def forward(self, x: torch.Tensor, amax: torch.Tensor | None = None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, amax: torch.Tensor | None = None,
+                dx_consumer: "MossLinear | None" = None) -> torch.Tensor:
+        """``amax``: max|x| from x's producer; ``dx_consumer``: the MossLinear that
+        quantizes dX as its output-gradient (gets max|dX| from the dgrad epilogue)."""
         if self.schedule is None:
             self.init_fp8()
         if self.fp8_pending is not None:
             pending, self.fp8_pending = self.fp8_pending, None
             pending()
-        return MossLinearFunction.apply(x, self.weight, self, amax)
+        return MossLinearFunction.apply(x, self.weight, self, amax, dx_consumer)
 
     def extra_repr(self) -> str:
         return f"in_features={self.in_features}, out_features={self.out_features}, fp8=e4m3(mx2 act, per-tensor W)"

@@ -12,8 +12,9 @@ backward gradient:
 The glue ops are producer kernels (producers.py) as in the Llama decoder:
 each writes the amax of the tensor it makes, so the quantizers of a/r/h (fwd)
 and of the qkv/gate_up/down output-gradients run in producer-amax mode (one
-read, no reduction).  Only x (the step's input) and o's output-gradient (the
-gate_up dgrad GEMM's output) are quantized with the in-kernel amax.
+read, no reduction); o's output-gradient is the gate_up dgrad GEMM's output,
+whose amax comes from the GEMM epilogue.  Only x (the step's input) is
+quantized with the in-kernel amax.
 
 The residual branch does not back-propagate into the step input x (x's
 gradient is the QKV dgrad only): no autograd add of two gradient paths, so
@@ -51,7 +52,9 @@ class LayerStack(nn.Module):
         # input (x's gradient is the qkv dgrad alone), so no autograd sum of the two
         # paths runs: every kernel of the step is one of ours
         r, am = AddFn.apply(x.detach(), self.o(a, am))
-        h, am = SwiGLUFn.apply(self.gate_up(r, am), self.gate_up)
+        # gate_up's dX is O's output-gradient (AddFn passes it through): the dgrad
+        # epilogue hands O its amax
+        h, am = SwiGLUFn.apply(self.gate_up(r, am, dx_consumer=self.o), self.gate_up)
         return MeanSquareFn.apply(self.down(h, am), self.down)    # mean(y^2)
 
     def gemm_flops_per_token(self) -> int:

@@ -46,9 +46,17 @@ def test_argument_checks_precede_launch():
     # cols % 32 -> InvalidShapeError, checked before touching the device
     assert lib.moss_quant_mx2(fake, 1, 4, 33, fake, fake, None, None, None, None, None, None, fake, None) == 1
     # K % 128 -> shape error
-    assert lib.moss_gemm_mxf8(fake, fake, fake, None, fake, fake, fake, 1, 128, 128, 128, 96, 0, None) == 1
+    assert lib.moss_gemm_mxf8(fake, fake, fake, None, fake, fake, fake, 1, 128, 128, 128, 96, 0, None, None,
+                              None) == 1
     # accumulate into bf16 -> argument error
-    assert lib.moss_gemm_mxf8(fake, fake, fake, None, fake, fake, fake, 1, 128, 128, 128, 128, 1, None) == 3
+    assert lib.moss_gemm_mxf8(fake, fake, fake, None, fake, fake, fake, 1, 128, 128, 128, 128, 1, None, None,
+                              None) == 3
+    # amax epilogue with accumulate (the stored sum is not seen) -> argument error
+    assert lib.moss_gemm_mxf8(fake, fake, fake, None, fake, fake, fake, 0, 128, 128, 128, 128, 1, fake, fake,
+                              None) == 3
+    # amax epilogue needs a contiguous D (ldd == N)
+    assert lib.moss_gemm_mxf8(fake, fake, fake, None, fake, fake, fake, 1, 256, 128, 128, 128, 0, fake, fake,
+                              None) == 3
     # misaligned pointer -> alignment error
     odd = ctypes.c_void_p(17)
     assert lib.moss_amax(odd, 1, 64, fake, fake, None) == 6
