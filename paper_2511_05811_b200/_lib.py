@@ -286,7 +286,7 @@ def gemm(a, sfa, b, sfb, s_a, s_b, d, *, accumulate: bool = False, amax=None, fl
     with _Span("gemm", 2.0 * m * n * k):
         check(lib().moss_gemm_mxf8(a.data_ptr(), sfa.data_ptr(), b.data_ptr(), ptr(sfb), s_a.data_ptr(),
                                    s_b.data_ptr(), d.data_ptr(), dtype_code(d), d.stride(0), m, n, k,
-                                   int(accumulate), ptr(amax), ptr(flags), stream()),
+                                   int(accumulate), ptr(amax), flags.ptr if flags is not None else None, stream()),
               "moss_gemm_mxf8")
 
 

@@ -16,6 +16,7 @@
 // like its bits; NaN/Inf land above 0x7F800000 and the quantizer flags them).
 // The caller zeroes the amax word (stream-ordered memset in the launcher).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "host_utils.cuh"
@@ -207,6 +208,177 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_warp_kernel(const __nv_bfloat
             const uint4 ob = bf16x8_pack(a);
             *reinterpret_cast<uint4*>(y + row + c) = ob;
             m = max(m, absmax_bits_bf16(ob));
+        }
+    }
+    block_amax_commit(m, red_u, amax);
+}
+
+// ---- v2 (d % 1024 == 0, i.e. the 7B width 4096): a CTA of NT = d/32 threads
+// owns one row per iteration, each thread VPT = 4 strided 16-byte vectors
+// (32 elements: consecutive threads read consecutive 16 B, fully coalesced).
+// All of a row's loads (x and delta, or dy, x and d_res) are issued before any
+// math; ~4-5 CTAs per SM keep 100+ KB in flight per SM.  One __syncthreads per
+// row (the partial sums are double-buffered in shared memory).  The v1 warp
+// kernel held a whole 4096-wide row per warp in 237 registers at 8 warps/SM
+// and issued the delta loads one vector at a time (0.52 of HBM).
+template <int NT>
+__device__ __forceinline__ float row_sum_db(float v, float (&red)[2][NT / 32], int it) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31) == 0) red[it & 1][threadIdx.x >> 5] = v;
+    __syncthreads();
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) s += red[it & 1][i];
+    return s;
+}
+
+template <int NT, int VPT>
+__global__ void __launch_bounds__(NT) rmsnorm_fwd_v2_kernel(const __nv_bfloat16* __restrict__ x,
+                                                            const __nv_bfloat16* __restrict__ delta,
+                                                            __nv_bfloat16* __restrict__ x_out,
+                                                            const float* __restrict__ w, float eps,
+                                                            __nv_bfloat16* __restrict__ y, float* __restrict__ rstd,
+                                                            uint32_t* amax, int T, int d) {
+    __shared__ float red[2][NT / 32];
+    __shared__ uint32_t red_u[NT / 32];
+    const int tid = threadIdx.x;
+    float wv[VPT][8];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const int c = (i * NT + tid) * 8;
+        const float4 a = __ldg(reinterpret_cast<const float4*>(w + c));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(w + c + 4));
+        wv[i][0] = a.x; wv[i][1] = a.y; wv[i][2] = a.z; wv[i][3] = a.w;
+        wv[i][4] = b.x; wv[i][5] = b.y; wv[i][6] = b.z; wv[i][7] = b.w;
+    }
+    uint32_t m = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < T; t += gridDim.x, ++it) {
+        const int64_t row = (int64_t)t * d;
+        uint4 v[VPT], dd[VPT];
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) v[i] = *reinterpret_cast<const uint4*>(x + row + (i * NT + tid) * 8);
+        if (delta) {
+#pragma unroll
+            for (int i = 0; i < VPT; ++i) dd[i] = *reinterpret_cast<const uint4*>(delta + row + (i * NT + tid) * 8);
+        }
+        float ss = 0.f;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            float a[8];
+            unpack_bf16x8(v[i], a);
+            if (delta) {
+                float b[8];
+                unpack_bf16x8(dd[i], b);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) a[j] += b[j];
+                v[i] = bf16x8_pack(a);
+                *reinterpret_cast<uint4*>(x_out + row + (i * NT + tid) * 8) = v[i];
+                unpack_bf16x8(v[i], a);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ss = fmaf(a[j], a[j], ss);
+        }
+        ss = row_sum_db<NT>(ss, red, it);
+        const float r = rsqrtf(ss / (float)d + eps);
+        if (tid == 0) rstd[t] = r;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            float a[8];
+            unpack_bf16x8(v[i], a);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a[j] = a[j] * r * wv[i][j];
+            const uint4 ob = bf16x8_pack(a);
+            *reinterpret_cast<uint4*>(y + row + (i * NT + tid) * 8) = ob;
+            m = max(m, absmax_bits_bf16(ob));
+        }
+    }
+    block_amax_commit(m, red_u, amax);
+}
+
+template <int NT, int VPT>
+__global__ void __launch_bounds__(NT) rmsnorm_bwd_v2_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                            const __nv_bfloat16* __restrict__ x,
+                                                            const float* __restrict__ w,
+                                                            const float* __restrict__ rstd,
+                                                            const __nv_bfloat16* __restrict__ d_res,
+                                                            __nv_bfloat16* __restrict__ dx,
+                                                            float* __restrict__ dw_part, uint32_t* amax, int T,
+                                                            int d) {
+    __shared__ float red[2][NT / 32];
+    __shared__ uint32_t red_u[NT / 32];
+    const int tid = threadIdx.x;
+    float dwp[VPT][8];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dwp[i][j] = 0.f;
+    uint32_t m = 0;
+    const float inv_d = 1.0f / (float)d;
+    int it = 0;
+    for (int t = blockIdx.x; t < T; t += gridDim.x, ++it) {
+        const int64_t row = (int64_t)t * d;
+        uint4 yv[VPT], xv[VPT], rv[VPT];
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            yv[i] = *reinterpret_cast<const uint4*>(dy + row + (i * NT + tid) * 8);
+            xv[i] = *reinterpret_cast<const uint4*>(x + row + (i * NT + tid) * 8);
+        }
+        if (d_res) {
+#pragma unroll
+            for (int i = 0; i < VPT; ++i) rv[i] = *reinterpret_cast<const uint4*>(d_res + row + (i * NT + tid) * 8);
+        }
+        const float r = rstd[t];
+        float dot = 0.f;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            const int c = (i * NT + tid) * 8;
+            const float4 w0 = __ldg(reinterpret_cast<const float4*>(w + c));
+            const float4 w1 = __ldg(reinterpret_cast<const float4*>(w + c + 4));
+            const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            float dv[8], xh[8];
+            unpack_bf16x8(yv[i], dv);
+            unpack_bf16x8(xv[i], xh);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                xh[j] *= r;
+                dot = fmaf(dv[j] * wv[j], xh[j], dot);
+                dwp[i][j] = fmaf(dv[j], xh[j], dwp[i][j]);
+            }
+        }
+        dot = row_sum_db<NT>(dot, red, it) * inv_d;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            const int c = (i * NT + tid) * 8;
+            const float4 w0 = __ldg(reinterpret_cast<const float4*>(w + c));
+            const float4 w1 = __ldg(reinterpret_cast<const float4*>(w + c + 4));
+            const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            float dv[8], xh[8], o[8];
+            unpack_bf16x8(yv[i], dv);
+            unpack_bf16x8(xv[i], xh);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                xh[j] *= r;
+                o[j] = r * (dv[j] * wv[j] - xh[j] * dot);
+            }
+            if (d_res) {
+                float rr[8];
+                unpack_bf16x8(rv[i], rr);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) o[j] += rr[j];
+            }
+            const uint4 ob = bf16x8_pack(o);
+            *reinterpret_cast<uint4*>(dx + row + c) = ob;
+            m = max(m, absmax_bits_bf16(ob));
+        }
+    }
+    if (dw_part) {   // this CTA's column sums; reduced in a fixed order by rmsnorm_dw_reduce_kernel
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            float* dst = dw_part + (int64_t)blockIdx.x * d + (i * NT + tid) * 8;
+            reinterpret_cast<float4*>(dst)[0] = make_float4(dwp[i][0], dwp[i][1], dwp[i][2], dwp[i][3]);
+            reinterpret_cast<float4*>(dst)[1] = make_float4(dwp[i][4], dwp[i][5], dwp[i][6], dwp[i][7]);
         }
     }
     block_amax_commit(m, red_u, amax);
@@ -615,6 +787,17 @@ static int resident(K kern, int threads) {
     return occ;
 }
 
+// MOSS_RMS_V2 (A/B testing): 1 (default) 128 threads x 4 vectors per row, 2 = 256 x 2, 0 = the v1 kernels
+static int rms_v2_mode() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MOSS_RMS_V2");
+        v = e ? (e[0] - '0') : 1;
+        if (v < 0 || v > 2) v = 1;
+    }
+    return v;
+}
+
 static dim3 swiglu_grid(int64_t T, int64_t f) {
     const int64_t gx = (f / 8 + 255) / 256;
     const int64_t gy = std::min<int64_t>(T, std::max<int64_t>(1, (int64_t)sm_count() * 16 / gx));
@@ -628,6 +811,18 @@ static int amax_reset(uint32_t* amax, cudaStream_t st) {
 int launch_rmsnorm_fwd(const void* x, const void* delta, void* x_out, const float* w, float eps, void* y, float* rstd,
                        float* amax, int64_t T, int64_t d, cudaStream_t st) {
     if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
+    if (d == 4096 && rms_v2_mode() != 0) {
+        auto go = [&](auto kern, int nt) {
+            static int occ = resident(kern, nt);    // one static per kernel instance
+            const int grid = (int)std::min<int64_t>(T, (int64_t)sm_count() * occ);
+            kern<<<grid, nt, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)delta, (__nv_bfloat16*)x_out,
+                                      w, eps, (__nv_bfloat16*)y, rstd, reinterpret_cast<uint32_t*>(amax), (int)T,
+                                      (int)d);
+        };
+        if (rms_v2_mode() == 2) go(rmsnorm_fwd_v2_kernel<256, 2>, 256);
+        else go(rmsnorm_fwd_v2_kernel<128, 4>, 128);
+        return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+    }
     if (d % 256 == 0 && d / 256 <= 16) {
         auto warp_args = [&](auto kern) {
             static int occ = resident(kern, 256);
@@ -670,6 +865,11 @@ block_path:
 }
 
 static int rmsnorm_bwd_grid(int64_t T, int64_t d) {
+    if (d == 4096 && rms_v2_mode() != 0) {
+        static int occ1 = resident(rmsnorm_bwd_v2_kernel<128, 4>, 128);
+        static int occ2 = resident(rmsnorm_bwd_v2_kernel<256, 2>, 256);
+        return (int)std::min<int64_t>(T, (int64_t)sm_count() * (rms_v2_mode() == 2 ? occ2 : occ1));
+    }
     const int nt = (int)((d / 8 + 31) / 32 * 32);
     return (int)std::min<int64_t>(T, (int64_t)sm_count() * std::max(1, 1024 / nt));
 }
@@ -681,6 +881,17 @@ int launch_rmsnorm_bwd(const void* dy, const void* x, const float* w, const floa
     if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
     const int nt = (int)((d / 8 + 31) / 32 * 32);
     const int grid = rmsnorm_bwd_grid(T, d);
+    if (d == 4096 && rms_v2_mode() != 0) {
+        auto go = [&](auto kern, int ntv) {
+            kern<<<grid, ntv, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, w, rstd,
+                                       (const __nv_bfloat16*)d_res, (__nv_bfloat16*)dx, dw ? ws : nullptr,
+                                       reinterpret_cast<uint32_t*>(amax), (int)T, (int)d);
+        };
+        if (rms_v2_mode() == 2) go(rmsnorm_bwd_v2_kernel<256, 2>, 256);
+        else go(rmsnorm_bwd_v2_kernel<128, 4>, 128);
+        if (dw) rmsnorm_dw_reduce_kernel<<<(unsigned)((d + 63) / 64), 1024, 0, st>>>(ws, dw, grid, (int)d);
+        return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
+    }
     auto args = [&](auto kern) {
         kern<<<grid, nt, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, w, rstd,
                                   (const __nv_bfloat16*)d_res, (__nv_bfloat16*)dx, dw ? ws : nullptr,

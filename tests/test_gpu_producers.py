@@ -49,7 +49,7 @@ def test_rmsnorm_dw_deterministic():
         assert torch.equal(dx, outs[0][0]) and torch.equal(dw, outs[0][1])
 
 
-@pytest.mark.parametrize("T,d", [(64, 128), (256, 768), (512, 4096)])
+@pytest.mark.parametrize("T,d", [(64, 128), (256, 768), (512, 4096), (4096, 4096), (7, 4096)])
 @pytest.mark.parametrize("residual", [False, True])
 def test_rmsnorm_fwd_bwd(T, d, residual):
     torch.manual_seed(T + d)
