@@ -384,6 +384,220 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_v2_kernel(const __nv_bfloat16*
     block_amax_commit(m, red_u, amax);
 }
 
+// ---- v3 (d = NT*VPT*8): the v2 dataflow fed by a TMA bulk-copy ring.  Thread 0
+// streams whole input rows (cp.async.bulk, 8 KB each at d = 4096) into STAGES
+// shared-memory slots ahead of the compute, so every CTA keeps STAGES rows in
+// flight regardless of register pressure (v2 had one row in flight per CTA and
+// stalled between its load and store phases: 3.3-3.6 TB/s on the bwd).  The
+// slot is refilled right after the row-sum barrier (every thread has its
+// values in registers by then).
+template <int NIN, int STAGES>
+struct RowRing {
+    uint64_t* full;
+    uint8_t* slots;
+    int rowb;
+    __device__ __forceinline__ uint8_t* slot(int s) const { return slots + (size_t)s * NIN * rowb; }
+    __device__ __forceinline__ void issue(int s, const __nv_bfloat16* const (&src)[NIN], int64_t off) const {
+        mbar_arrive_expect_tx(&full[s], (uint32_t)(NIN * rowb));
+#pragma unroll
+        for (int k = 0; k < NIN; ++k)
+            if (src[k]) bulk_load(slot(s) + k * rowb, src[k] + off, (uint32_t)rowb, &full[s]);
+    }
+};
+
+template <int NT, int VPT, int STAGES>
+__global__ void __launch_bounds__(NT) rmsnorm_fwd_v3_kernel(const __nv_bfloat16* __restrict__ x,
+                                                            const __nv_bfloat16* __restrict__ delta,
+                                                            __nv_bfloat16* __restrict__ x_out,
+                                                            const float* __restrict__ w, float eps,
+                                                            __nv_bfloat16* __restrict__ y, float* __restrict__ rstd,
+                                                            uint32_t* amax, int T, int d) {
+    extern __shared__ __align__(128) uint8_t rs_smem[];
+    constexpr int ROWB = NT * VPT * 16;
+    __shared__ float red[2][NT / 32];
+    __shared__ uint32_t red_u[NT / 32];
+    __shared__ __align__(8) uint64_t full[STAGES];
+    const int tid = threadIdx.x, G = gridDim.x;
+    const int n = T > (int)blockIdx.x ? (T - (int)blockIdx.x + G - 1) / G : 0;
+    RowRing<2, STAGES> ring{full, rs_smem, ROWB};
+    // delta absent: the second input slot is simply not loaded (its bytes not expected)
+    const __nv_bfloat16* const src[2] = {x, delta};
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int nin_bytes = delta ? 2 * ROWB : ROWB;
+    auto issue = [&](int j) {
+        const int s = j % STAGES;
+        mbar_arrive_expect_tx(&full[s], (uint32_t)nin_bytes);
+        const int64_t off = (int64_t)((int)blockIdx.x + j * G) * d;
+        bulk_load(ring.slot(s), src[0] + off, ROWB, &full[s]);
+        if (delta) bulk_load(ring.slot(s) + ROWB, src[1] + off, ROWB, &full[s]);
+    };
+    if (tid == 0)
+        for (int j = 0; j < min(n, STAGES); ++j) issue(j);
+    float wv[VPT][8];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const int c = (i * NT + tid) * 8;
+        const float4 a = __ldg(reinterpret_cast<const float4*>(w + c));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(w + c + 4));
+        wv[i][0] = a.x; wv[i][1] = a.y; wv[i][2] = a.z; wv[i][3] = a.w;
+        wv[i][4] = b.x; wv[i][5] = b.y; wv[i][6] = b.z; wv[i][7] = b.w;
+    }
+    uint32_t m = 0, par = 0;
+    for (int j = 0; j < n; ++j) {
+        const int s = j % STAGES, t = (int)blockIdx.x + j * G;
+        const int64_t row = (int64_t)t * d;
+        mbar_wait(&full[s], (par >> s) & 1u);
+        par ^= 1u << s;
+        const uint32_t base = smem_u32(ring.slot(s));
+        uint4 v[VPT];
+        float ss = 0.f;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            v[i] = lds128(base + (i * NT + tid) * 16);
+            float a[8];
+            unpack_bf16x8(v[i], a);
+            if (delta) {
+                float b[8];
+                unpack_bf16x8(lds128(base + ROWB + (i * NT + tid) * 16), b);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) a[k] += b[k];
+                v[i] = bf16x8_pack(a);
+                *reinterpret_cast<uint4*>(x_out + row + (i * NT + tid) * 8) = v[i];
+                unpack_bf16x8(v[i], a);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) ss = fmaf(a[k], a[k], ss);
+        }
+        ss = row_sum_db<NT>(ss, red, j);             // every thread has read slot s
+        if (tid == 0 && j + STAGES < n) issue(j + STAGES);
+        const float r = rsqrtf(ss / (float)d + eps);
+        if (tid == 0) rstd[t] = r;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            float a[8];
+            unpack_bf16x8(v[i], a);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) a[k] = a[k] * r * wv[i][k];
+            const uint4 ob = bf16x8_pack(a);
+            *reinterpret_cast<uint4*>(y + row + (i * NT + tid) * 8) = ob;
+            m = max(m, absmax_bits_bf16(ob));
+        }
+    }
+    block_amax_commit(m, red_u, amax);
+}
+
+template <int NT, int VPT, int STAGES>
+__global__ void __launch_bounds__(NT) rmsnorm_bwd_v3_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                            const __nv_bfloat16* __restrict__ x,
+                                                            const float* __restrict__ w,
+                                                            const float* __restrict__ rstd,
+                                                            const __nv_bfloat16* __restrict__ d_res,
+                                                            __nv_bfloat16* __restrict__ dx,
+                                                            float* __restrict__ dw_part, uint32_t* amax, int T,
+                                                            int d) {
+    extern __shared__ __align__(128) uint8_t rs_smem[];
+    constexpr int ROWB = NT * VPT * 16;
+    __shared__ float red[2][NT / 32];
+    __shared__ uint32_t red_u[NT / 32];
+    __shared__ __align__(8) uint64_t full[STAGES];
+    const int tid = threadIdx.x, G = gridDim.x;
+    const int n = T > (int)blockIdx.x ? (T - (int)blockIdx.x + G - 1) / G : 0;
+    RowRing<3, STAGES> ring{full, rs_smem, ROWB};
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int nbytes = d_res ? 3 * ROWB : 2 * ROWB;
+    auto issue = [&](int j) {
+        const int s = j % STAGES;
+        mbar_arrive_expect_tx(&full[s], (uint32_t)nbytes);
+        const int64_t off = (int64_t)((int)blockIdx.x + j * G) * d;
+        bulk_load(ring.slot(s), dy + off, ROWB, &full[s]);
+        bulk_load(ring.slot(s) + ROWB, x + off, ROWB, &full[s]);
+        if (d_res) bulk_load(ring.slot(s) + 2 * ROWB, d_res + off, ROWB, &full[s]);
+    };
+    if (tid == 0)
+        for (int j = 0; j < min(n, STAGES); ++j) issue(j);
+    float dwp[VPT][8];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dwp[i][k] = 0.f;
+    uint32_t m = 0, par = 0;
+    const float inv_d = 1.0f / (float)d;
+    for (int j = 0; j < n; ++j) {
+        const int s = j % STAGES, t = (int)blockIdx.x + j * G;
+        const int64_t row = (int64_t)t * d;
+        const float r = rstd[t];
+        mbar_wait(&full[s], (par >> s) & 1u);
+        par ^= 1u << s;
+        const uint32_t base = smem_u32(ring.slot(s));
+        uint4 yv[VPT], xv[VPT], rv[VPT];
+        float dot = 0.f;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            const int c = (i * NT + tid) * 8;
+            yv[i] = lds128(base + (i * NT + tid) * 16);
+            xv[i] = lds128(base + ROWB + (i * NT + tid) * 16);
+            if (d_res) rv[i] = lds128(base + 2 * ROWB + (i * NT + tid) * 16);
+            const float4 w0 = __ldg(reinterpret_cast<const float4*>(w + c));
+            const float4 w1 = __ldg(reinterpret_cast<const float4*>(w + c + 4));
+            const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            float dv[8], xh[8];
+            unpack_bf16x8(yv[i], dv);
+            unpack_bf16x8(xv[i], xh);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                xh[k] *= r;
+                dot = fmaf(dv[k] * wv[k], xh[k], dot);
+                dwp[i][k] = fmaf(dv[k], xh[k], dwp[i][k]);
+            }
+        }
+        dot = row_sum_db<NT>(dot, red, j) * inv_d;      // every thread has read slot s
+        if (tid == 0 && j + STAGES < n) issue(j + STAGES);
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            const int c = (i * NT + tid) * 8;
+            const float4 w0 = __ldg(reinterpret_cast<const float4*>(w + c));
+            const float4 w1 = __ldg(reinterpret_cast<const float4*>(w + c + 4));
+            const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            float dv[8], xh[8], o[8];
+            unpack_bf16x8(yv[i], dv);
+            unpack_bf16x8(xv[i], xh);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                xh[k] *= r;
+                o[k] = r * (dv[k] * wv[k] - xh[k] * dot);
+            }
+            if (d_res) {
+                float rr[8];
+                unpack_bf16x8(rv[i], rr);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) o[k] += rr[k];
+            }
+            const uint4 ob = bf16x8_pack(o);
+            *reinterpret_cast<uint4*>(dx + row + c) = ob;
+            m = max(m, absmax_bits_bf16(ob));
+        }
+    }
+    if (dw_part) {
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            float* dst = dw_part + (int64_t)blockIdx.x * d + (i * NT + tid) * 8;
+            reinterpret_cast<float4*>(dst)[0] = make_float4(dwp[i][0], dwp[i][1], dwp[i][2], dwp[i][3]);
+            reinterpret_cast<float4*>(dst)[1] = make_float4(dwp[i][4], dwp[i][5], dwp[i][6], dwp[i][7]);
+        }
+    }
+    block_amax_commit(m, red_u, amax);
+}
+
 // backward: xh = f32(x') * rstd; gw = f32(dy) * w; c = mean(gw * xh)
 //   dx = bf16( rstd * (gw - xh * c) + f32(d_res) )   (d_res: gradient arriving
 //        through the residual stream; null = 0)
@@ -787,15 +1001,32 @@ static int resident(K kern, int threads) {
     return occ;
 }
 
-// MOSS_RMS_V2 (A/B testing): 1 (default) 128 threads x 4 vectors per row, 2 = 256 x 2, 0 = the v1 kernels
+// MOSS_RMS_V2 (A/B testing, d = 4096): 3 (default) the TMA-ring v3 kernels, 1 = v2 128 threads x 4
+// vectors per row, 2 = v2 256 x 2, 0 = the v1 kernels
 static int rms_v2_mode() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("MOSS_RMS_V2");
-        v = e ? (e[0] - '0') : 1;
-        if (v < 0 || v > 2) v = 1;
+        v = e ? (e[0] - '0') : 3;
+        if (v < 0 || v > 3) v = 3;
     }
     return v;
+}
+constexpr int RMS3_FWD_STAGES = 4, RMS3_BWD_STAGES = 3;
+constexpr int RMS3_FWD_SMEM = RMS3_FWD_STAGES * 2 * 4096 * 2;    // x + delta rows, bf16
+constexpr int RMS3_BWD_SMEM = RMS3_BWD_STAGES * 3 * 4096 * 2;    // dy + x + d_res rows
+
+static int rms3_bwd_occ() {
+    static int occ_dev[kMaxDevices] = {};
+    static bool optin[kMaxDevices] = {};
+    const int dev = current_device();
+    auto kern = rmsnorm_bwd_v3_kernel<128, 4, RMS3_BWD_STAGES>;
+    if (!smem_optin(kern, RMS3_BWD_SMEM, optin)) return 0;
+    if (!occ_dev[dev] &&
+        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_dev[dev], kern, 128, RMS3_BWD_SMEM) != cudaSuccess ||
+         occ_dev[dev] < 1))
+        occ_dev[dev] = 1;
+    return occ_dev[dev];
 }
 
 static dim3 swiglu_grid(int64_t T, int64_t f) {
@@ -819,8 +1050,25 @@ int launch_rmsnorm_fwd(const void* x, const void* delta, void* x_out, const floa
                                       w, eps, (__nv_bfloat16*)y, rstd, reinterpret_cast<uint32_t*>(amax), (int)T,
                                       (int)d);
         };
-        if (rms_v2_mode() == 2) go(rmsnorm_fwd_v2_kernel<256, 2>, 256);
-        else go(rmsnorm_fwd_v2_kernel<128, 4>, 128);
+        if (rms_v2_mode() == 3) {
+            auto kern = rmsnorm_fwd_v3_kernel<128, 4, RMS3_FWD_STAGES>;
+            static bool optin[kMaxDevices] = {};
+            static int occ_dev[kMaxDevices] = {};
+            const int dev = current_device();
+            if (!smem_optin(kern, RMS3_FWD_SMEM, optin)) return MOSS_ERR_CUDA;
+            if (!occ_dev[dev] && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_dev[dev], kern, 128,
+                                                                                RMS3_FWD_SMEM) != cudaSuccess ||
+                                  occ_dev[dev] < 1))
+                occ_dev[dev] = 1;
+            const int grid = (int)std::min<int64_t>(T, (int64_t)sm_count() * occ_dev[dev]);
+            kern<<<grid, 128, RMS3_FWD_SMEM, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)delta,
+                                                   (__nv_bfloat16*)x_out, w, eps, (__nv_bfloat16*)y, rstd,
+                                                   reinterpret_cast<uint32_t*>(amax), (int)T, (int)d);
+        } else if (rms_v2_mode() == 2) {
+            go(rmsnorm_fwd_v2_kernel<256, 2>, 256);
+        } else {
+            go(rmsnorm_fwd_v2_kernel<128, 4>, 128);
+        }
         return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
     }
     if (d % 256 == 0 && d / 256 <= 16) {
@@ -868,7 +1116,8 @@ static int rmsnorm_bwd_grid(int64_t T, int64_t d) {
     if (d == 4096 && rms_v2_mode() != 0) {
         static int occ1 = resident(rmsnorm_bwd_v2_kernel<128, 4>, 128);
         static int occ2 = resident(rmsnorm_bwd_v2_kernel<256, 2>, 256);
-        return (int)std::min<int64_t>(T, (int64_t)sm_count() * (rms_v2_mode() == 2 ? occ2 : occ1));
+        const int occ = rms_v2_mode() == 3 ? std::max(1, rms3_bwd_occ()) : rms_v2_mode() == 2 ? occ2 : occ1;
+        return (int)std::min<int64_t>(T, (int64_t)sm_count() * occ);
     }
     const int nt = (int)((d / 8 + 31) / 32 * 32);
     return (int)std::min<int64_t>(T, (int64_t)sm_count() * std::max(1, 1024 / nt));
@@ -887,8 +1136,16 @@ int launch_rmsnorm_bwd(const void* dy, const void* x, const float* w, const floa
                                        (const __nv_bfloat16*)d_res, (__nv_bfloat16*)dx, dw ? ws : nullptr,
                                        reinterpret_cast<uint32_t*>(amax), (int)T, (int)d);
         };
-        if (rms_v2_mode() == 2) go(rmsnorm_bwd_v2_kernel<256, 2>, 256);
-        else go(rmsnorm_bwd_v2_kernel<128, 4>, 128);
+        if (rms_v2_mode() == 3) {
+            if (!rms3_bwd_occ()) return MOSS_ERR_CUDA;
+            rmsnorm_bwd_v3_kernel<128, 4, RMS3_BWD_STAGES><<<grid, 128, RMS3_BWD_SMEM, st>>>(
+                (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, w, rstd, (const __nv_bfloat16*)d_res,
+                (__nv_bfloat16*)dx, dw ? ws : nullptr, reinterpret_cast<uint32_t*>(amax), (int)T, (int)d);
+        } else if (rms_v2_mode() == 2) {
+            go(rmsnorm_bwd_v2_kernel<256, 2>, 256);
+        } else {
+            go(rmsnorm_bwd_v2_kernel<128, 4>, 128);
+        }
         if (dw) rmsnorm_dw_reduce_kernel<<<(unsigned)((d + 63) / 64), 1024, 0, st>>>(ws, dw, grid, (int)d);
         return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
     }
