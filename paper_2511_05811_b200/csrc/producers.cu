@@ -1001,14 +1001,14 @@ static int resident(K kern, int threads) {
     return occ;
 }
 
-// MOSS_RMS_V2 (A/B testing, d = 4096): 3 (default) the TMA-ring v3 kernels, 1 = v2 128 threads x 4
-// vectors per row, 2 = v2 256 x 2, 0 = the v1 kernels
+// MOSS_RMS_V2 (A/B testing, d = 4096): 4 (default) the TMA-ring v3 kernels with 256 threads x 2
+// vectors per row, 3 = v3 with 128 x 4, 1 = v2 128 x 4, 2 = v2 256 x 2, 0 = the v1 kernels
 static int rms_v2_mode() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("MOSS_RMS_V2");
-        v = e ? (e[0] - '0') : 3;
-        if (v < 0 || v > 3) v = 3;
+        v = e ? (e[0] - '0') : 4;
+        if (v < 0 || v > 4) v = 4;
     }
     return v;
 }
@@ -1016,18 +1016,20 @@ constexpr int RMS3_FWD_STAGES = 4, RMS3_BWD_STAGES = 3;
 constexpr int RMS3_FWD_SMEM = RMS3_FWD_STAGES * 2 * 4096 * 2;    // x + delta rows, bf16
 constexpr int RMS3_BWD_SMEM = RMS3_BWD_STAGES * 3 * 4096 * 2;    // dy + x + d_res rows
 
-static int rms3_bwd_occ() {
+template <int NT>
+static int rms3_bwd_occ_t() {
     static int occ_dev[kMaxDevices] = {};
     static bool optin[kMaxDevices] = {};
     const int dev = current_device();
-    auto kern = rmsnorm_bwd_v3_kernel<128, 4, RMS3_BWD_STAGES>;
+    auto kern = rmsnorm_bwd_v3_kernel<NT, 512 / NT, RMS3_BWD_STAGES>;
     if (!smem_optin(kern, RMS3_BWD_SMEM, optin)) return 0;
     if (!occ_dev[dev] &&
-        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_dev[dev], kern, 128, RMS3_BWD_SMEM) != cudaSuccess ||
+        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_dev[dev], kern, NT, RMS3_BWD_SMEM) != cudaSuccess ||
          occ_dev[dev] < 1))
         occ_dev[dev] = 1;
     return occ_dev[dev];
 }
+static int rms3_bwd_occ() { return rms_v2_mode() == 4 ? rms3_bwd_occ_t<256>() : rms3_bwd_occ_t<128>(); }
 
 static dim3 swiglu_grid(int64_t T, int64_t f) {
     const int64_t gx = (f / 8 + 255) / 256;
@@ -1050,20 +1052,25 @@ int launch_rmsnorm_fwd(const void* x, const void* delta, void* x_out, const floa
                                       w, eps, (__nv_bfloat16*)y, rstd, reinterpret_cast<uint32_t*>(amax), (int)T,
                                       (int)d);
         };
-        if (rms_v2_mode() == 3) {
-            auto kern = rmsnorm_fwd_v3_kernel<128, 4, RMS3_FWD_STAGES>;
-            static bool optin[kMaxDevices] = {};
-            static int occ_dev[kMaxDevices] = {};
-            const int dev = current_device();
-            if (!smem_optin(kern, RMS3_FWD_SMEM, optin)) return MOSS_ERR_CUDA;
-            if (!occ_dev[dev] && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_dev[dev], kern, 128,
-                                                                                RMS3_FWD_SMEM) != cudaSuccess ||
-                                  occ_dev[dev] < 1))
-                occ_dev[dev] = 1;
-            const int grid = (int)std::min<int64_t>(T, (int64_t)sm_count() * occ_dev[dev]);
-            kern<<<grid, 128, RMS3_FWD_SMEM, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)delta,
-                                                   (__nv_bfloat16*)x_out, w, eps, (__nv_bfloat16*)y, rstd,
-                                                   reinterpret_cast<uint32_t*>(amax), (int)T, (int)d);
+        if (rms_v2_mode() >= 3) {
+            auto go3 = [&](auto kern, int nt) {
+                static bool optin[kMaxDevices] = {};
+                static int occ_dev[kMaxDevices] = {};
+                const int dev = current_device();
+                if (!smem_optin(kern, RMS3_FWD_SMEM, optin)) return false;
+                if (!occ_dev[dev] && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_dev[dev], kern, nt,
+                                                                                    RMS3_FWD_SMEM) != cudaSuccess ||
+                                      occ_dev[dev] < 1))
+                    occ_dev[dev] = 1;
+                const int grid = (int)std::min<int64_t>(T, (int64_t)sm_count() * occ_dev[dev]);
+                kern<<<grid, nt, RMS3_FWD_SMEM, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)delta,
+                                                      (__nv_bfloat16*)x_out, w, eps, (__nv_bfloat16*)y, rstd,
+                                                      reinterpret_cast<uint32_t*>(amax), (int)T, (int)d);
+                return true;
+            };
+            const bool ok = rms_v2_mode() == 4 ? go3(rmsnorm_fwd_v3_kernel<256, 2, RMS3_FWD_STAGES>, 256)
+                                               : go3(rmsnorm_fwd_v3_kernel<128, 4, RMS3_FWD_STAGES>, 128);
+            if (!ok) return MOSS_ERR_CUDA;
         } else if (rms_v2_mode() == 2) {
             go(rmsnorm_fwd_v2_kernel<256, 2>, 256);
         } else {
@@ -1116,7 +1123,7 @@ static int rmsnorm_bwd_grid(int64_t T, int64_t d) {
     if (d == 4096 && rms_v2_mode() != 0) {
         static int occ1 = resident(rmsnorm_bwd_v2_kernel<128, 4>, 128);
         static int occ2 = resident(rmsnorm_bwd_v2_kernel<256, 2>, 256);
-        const int occ = rms_v2_mode() == 3 ? std::max(1, rms3_bwd_occ()) : rms_v2_mode() == 2 ? occ2 : occ1;
+        const int occ = rms_v2_mode() >= 3 ? std::max(1, rms3_bwd_occ()) : rms_v2_mode() == 2 ? occ2 : occ1;
         return (int)std::min<int64_t>(T, (int64_t)sm_count() * occ);
     }
     const int nt = (int)((d / 8 + 31) / 32 * 32);
@@ -1136,11 +1143,16 @@ int launch_rmsnorm_bwd(const void* dy, const void* x, const float* w, const floa
                                        (const __nv_bfloat16*)d_res, (__nv_bfloat16*)dx, dw ? ws : nullptr,
                                        reinterpret_cast<uint32_t*>(amax), (int)T, (int)d);
         };
-        if (rms_v2_mode() == 3) {
+        if (rms_v2_mode() >= 3) {
             if (!rms3_bwd_occ()) return MOSS_ERR_CUDA;
-            rmsnorm_bwd_v3_kernel<128, 4, RMS3_BWD_STAGES><<<grid, 128, RMS3_BWD_SMEM, st>>>(
-                (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, w, rstd, (const __nv_bfloat16*)d_res,
-                (__nv_bfloat16*)dx, dw ? ws : nullptr, reinterpret_cast<uint32_t*>(amax), (int)T, (int)d);
+            auto go3 = [&](auto kern, int ntv) {
+                kern<<<grid, ntv, RMS3_BWD_SMEM, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, w, rstd,
+                                                       (const __nv_bfloat16*)d_res, (__nv_bfloat16*)dx,
+                                                       dw ? ws : nullptr, reinterpret_cast<uint32_t*>(amax), (int)T,
+                                                       (int)d);
+            };
+            if (rms_v2_mode() == 4) go3(rmsnorm_bwd_v3_kernel<256, 2, RMS3_BWD_STAGES>, 256);
+            else go3(rmsnorm_bwd_v3_kernel<128, 4, RMS3_BWD_STAGES>, 128);
         } else if (rms_v2_mode() == 2) {
             go(rmsnorm_bwd_v2_kernel<256, 2>, 256);
         } else {
