@@ -205,10 +205,12 @@ int64_t moss_rmsnorm_bwd_workspace_bytes(int64_t T, int64_t d);
 int moss_swiglu_fwd(const void* gu, void* h, float* amax, int64_t T, int64_t f, void* stream);
 /* dgu = [dh up silu'(gate) | dh silu(gate)] */
 int moss_swiglu_bwd(const void* dh, const void* gu, void* dgu, float* amax, int64_t T, int64_t f, void* stream);
-/* RoPE: qkv [B, S, 3, H, hd] -> q, k, v [B, H, S, hd], q/k pairs (2i, 2i+1)
- * rotated by cos/sin [S_max, hd/2] (f32) at position s */
+/* RoPE: qkv [B, S, 3, H, hd] -> q, k, v, q/k pairs (2i, 2i+1) rotated by
+ * cos/sin [S_max, hd/2] (f32) at position s.  q, k, v memory: [B, H, S, hd]
+ * (bshd = 0) or [B, S, H, hd] (bshd = 1; SDPA then returns its output in that
+ * layout and the O projection reads it without a transpose copy). */
 int moss_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q, void* k, void* v, int64_t B,
-                  int64_t S, int64_t H, int64_t hd, void* stream);
+                  int64_t S, int64_t H, int64_t hd, int bshd, void* stream);
 /* Elementwise glue producers (bf16, f32 math), each writing max|out| to *amax:
  * mode 0 sum3:   out [T, d] = x[:, 0:d] + x[:, d:2d] + x[:, 2d:3d]   (x [T, 3d])
  * mode 1 bcast3: out [T, 3d] = [x, x, x]                              (x [T, d])
@@ -228,9 +230,10 @@ int moss_cross_entropy_fwd(const void* logits, const int64_t* targets, float* ls
                            void* stream);
 int moss_cross_entropy_bwd(const void* logits, const int64_t* targets, const float* lse, const float* scale,
                            void* dlogits, int64_t T, int64_t V, void* stream);
-/* dq, dk, dv [B, H, S, hd] -> dqkv [B, S, 3, H, hd] (inverse rotation) */
+/* dq, dk, dv (memory [B, H, S, hd] or, bshd = 1, [B, S, H, hd]) -> dqkv [B, S, 3, H, hd]
+ * (inverse rotation) */
 int moss_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
-                  float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, void* stream);
+                  float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, int bshd, void* stream);
 
 
 /* ---------------------------------------------------------------------------

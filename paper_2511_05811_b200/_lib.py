@@ -42,8 +42,8 @@ _SIGS = {
     "moss_rmsnorm_bwd_workspace_bytes": (_I64, [_I64, _I64]),
     "moss_swiglu_fwd": (_I, [_P, _P, _P, _I64, _I64, _P]),
     "moss_swiglu_bwd": (_I, [_P, _P, _P, _P, _I64, _I64, _P]),
-    "moss_rope_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
-    "moss_rope_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P]),
+    "moss_rope_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I, _P]),
+    "moss_rope_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I, _P]),
     "moss_cross_entropy_fwd": (_I, [_P, _P, _P, _P, _I64, _I64, _P]),
     "moss_glue": (_I, [_I, _P, _P, _P, _F, _P, _P, _I64, _I64, _P]),
     "moss_gemm_mxf8_bkn": (_I, [_P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _P, _P]),
@@ -373,17 +373,18 @@ def swiglu_bwd(dh, gu, dgu, amax) -> None:
               "moss_swiglu_bwd")
 
 
-def rope_fwd(qkv, cos, sin, q, k, v, B: int, S: int, H: int, hd: int) -> None:
+def rope_fwd(qkv, cos, sin, q, k, v, B: int, S: int, H: int, hd: int, bshd: bool = False) -> None:
+    """q, k, v memory [B, H, S, hd] or (bshd) [B, S, H, hd]."""
     _bf16(qkv, "qkv")
     with _Span("producer", B * S * 3 * H * hd * 4):
         check(lib().moss_rope_fwd(qkv.data_ptr(), cos.data_ptr(), sin.data_ptr(), q.data_ptr(), k.data_ptr(),
-                                  v.data_ptr(), B, S, H, hd, stream()), "moss_rope_fwd")
+                                  v.data_ptr(), B, S, H, hd, int(bshd), stream()), "moss_rope_fwd")
 
 
-def rope_bwd(dq, dk, dv, cos, sin, dqkv, amax, B: int, S: int, H: int, hd: int) -> None:
+def rope_bwd(dq, dk, dv, cos, sin, dqkv, amax, B: int, S: int, H: int, hd: int, bshd: bool = False) -> None:
     with _Span("producer", B * S * 3 * H * hd * 4):
         check(lib().moss_rope_bwd(dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), cos.data_ptr(), sin.data_ptr(),
-                                  dqkv.data_ptr(), ptr(amax), B, S, H, hd, stream()), "moss_rope_bwd")
+                                  dqkv.data_ptr(), ptr(amax), B, S, H, hd, int(bshd), stream()), "moss_rope_bwd")
 
 
 def quant_per_group(x2d, codes, scales, flags: FlagWord, group: int = 128) -> None:

@@ -35,9 +35,9 @@ int64_t rmsnorm_bwd_workspace(int64_t T, int64_t d);
 int launch_swiglu_fwd(const void* gu, void* h, float* amax, int64_t T, int64_t f, cudaStream_t st);
 int launch_swiglu_bwd(const void* dh, const void* gu, void* dgu, float* amax, int64_t T, int64_t f, cudaStream_t st);
 int launch_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q, void* k, void* v, int64_t B,
-                    int64_t S, int64_t H, int64_t hd, cudaStream_t st);
+                    int64_t S, int64_t H, int64_t hd, int bshd, cudaStream_t st);
 int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
-                    float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, cudaStream_t st);
+                    float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, int bshd, cudaStream_t st);
 int launch_glue(int mode, const void* x, const void* y, const float* scale, float alpha, void* out, float* amax,
                 int64_t T, int64_t d, cudaStream_t st);
 int launch_sumsq(const void* x, int64_t n, float scale, float* acc, float* parts, cudaStream_t st);
@@ -231,19 +231,19 @@ int moss_swiglu_bwd(const void* dh, const void* gu, void* dgu, float* amax, int6
 }
 
 int moss_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q, void* k, void* v, int64_t B,
-                  int64_t S, int64_t H, int64_t hd, void* stream) {
+                  int64_t S, int64_t H, int64_t hd, int bshd, void* stream) {
     if (B <= 0 || S <= 0 || H <= 0 || hd <= 0 || hd % 8) return MOSS_ERR_SHAPE;
     if (!qkv || !cosv || !sinv || !q || !k || !v) return MOSS_ERR_ARGUMENT;
     if (!al16(qkv) || !al16(cosv) || !al16(sinv) || !al16(q) || !al16(k) || !al16(v)) return MOSS_ERR_ALIGN;
-    return moss::launch_rope_fwd(qkv, cosv, sinv, q, k, v, B, S, H, hd, (cudaStream_t)stream);
+    return moss::launch_rope_fwd(qkv, cosv, sinv, q, k, v, B, S, H, hd, bshd != 0, (cudaStream_t)stream);
 }
 
 int moss_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
-                  float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, void* stream) {
+                  float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, int bshd, void* stream) {
     if (B <= 0 || S <= 0 || H <= 0 || hd <= 0 || hd % 8) return MOSS_ERR_SHAPE;
     if (!dq || !dk || !dv || !cosv || !sinv || !dqkv) return MOSS_ERR_ARGUMENT;
     if (!al16(dq) || !al16(dk) || !al16(dv) || !al16(cosv) || !al16(sinv) || !al16(dqkv)) return MOSS_ERR_ALIGN;
-    return moss::launch_rope_bwd(dq, dk, dv, cosv, sinv, dqkv, amax, B, S, H, hd, (cudaStream_t)stream);
+    return moss::launch_rope_bwd(dq, dk, dv, cosv, sinv, dqkv, amax, B, S, H, hd, bshd != 0, (cudaStream_t)stream);
 }
 
 int moss_glue(int mode, const void* x, const void* y, const float* scale, float alpha, void* out, float* amax,

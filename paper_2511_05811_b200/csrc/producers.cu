@@ -760,8 +760,11 @@ __global__ void __launch_bounds__(256) swiglu_bwd_kernel(const __nv_bfloat16* __
 __global__ void __launch_bounds__(256) rope_fwd_kernel(const __nv_bfloat16* __restrict__ qkv,
                                                        const float* __restrict__ cosv, const float* __restrict__ sinv,
                                                        __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ k,
-                                                       __nv_bfloat16* __restrict__ v, int B, int S, int H, int hd) {
-    // blockIdx.x = token (b, s); (blockIdx.y, thread) cover the H*hd/8 vectors of q, k and v
+                                                       __nv_bfloat16* __restrict__ v, int B, int S, int H, int hd,
+                                                       int bshd) {
+    // blockIdx.x = token (b, s); (blockIdx.y, thread) cover the H*hd/8 vectors of q, k and v;
+    // q, k, v are [B, H, S, hd] contiguous (bshd = 0) or [B, S, H, hd] memory (bshd = 1: what
+    // cuDNN SDPA keeps for its output, so the O projection reads it without a transpose copy)
     const int vh = hd / 8;
     const int i = blockIdx.y * blockDim.x + threadIdx.x;
     if (i >= H * vh) return;
@@ -769,7 +772,7 @@ __global__ void __launch_bounds__(256) rope_fwd_kernel(const __nv_bfloat16* __re
     const int s = bs % S, b = bs / S;
     const int h = i / vh, j = i - h * vh;
     const int64_t src = (int64_t)bs * 3 * H * hd + (int64_t)i * 8;
-    const int64_t dst = (((int64_t)b * H + h) * S + s) * hd + j * 8;
+    const int64_t dst = bshd ? (int64_t)bs * H * hd + (int64_t)i * 8 : (((int64_t)b * H + h) * S + s) * hd + j * 8;
     const float4 c4 = *reinterpret_cast<const float4*>(cosv + (int64_t)s * (hd / 2) + j * 4);
     const float4 s4 = *reinterpret_cast<const float4*>(sinv + (int64_t)s * (hd / 2) + j * 4);
     const float cs[4] = {c4.x, c4.y, c4.z, c4.w}, sn[4] = {s4.x, s4.y, s4.z, s4.w};
@@ -795,7 +798,7 @@ __global__ void __launch_bounds__(256) rope_bwd_kernel(const __nv_bfloat16* __re
                                                        const __nv_bfloat16* __restrict__ dv,
                                                        const float* __restrict__ cosv, const float* __restrict__ sinv,
                                                        __nv_bfloat16* __restrict__ dqkv, uint32_t* amax, int B, int S,
-                                                       int H, int hd) {
+                                                       int H, int hd, int bshd) {
     __shared__ uint32_t red_u[8];
     const int vh = hd / 8;
     const int i = blockIdx.y * blockDim.x + threadIdx.x;
@@ -805,7 +808,7 @@ __global__ void __launch_bounds__(256) rope_bwd_kernel(const __nv_bfloat16* __re
         const int s = bs % S, b = bs / S;
         const int h = i / vh, j = i - h * vh;
         const int64_t dst = (int64_t)bs * 3 * H * hd + (int64_t)i * 8;
-        const int64_t src = (((int64_t)b * H + h) * S + s) * hd + j * 8;
+        const int64_t src = bshd ? (int64_t)bs * H * hd + (int64_t)i * 8 : (((int64_t)b * H + h) * S + s) * hd + j * 8;
         const float4 c4 = *reinterpret_cast<const float4*>(cosv + (int64_t)s * (hd / 2) + j * 4);
         const float4 s4 = *reinterpret_cast<const float4*>(sinv + (int64_t)s * (hd / 2) + j * 4);
         const float cs[4] = {c4.x, c4.y, c4.z, c4.w}, sn[4] = {s4.x, s4.y, s4.z, s4.w};
@@ -1196,19 +1199,19 @@ int launch_swiglu_bwd(const void* dh, const void* gu, void* dgu, float* amax, in
 }
 
 int launch_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q, void* k, void* v, int64_t B,
-                    int64_t S, int64_t H, int64_t hd, cudaStream_t st) {
+                    int64_t S, int64_t H, int64_t hd, int bshd, cudaStream_t st) {
     rope_fwd_kernel<<<dim3((unsigned)(B * S), (unsigned)((H * (hd / 8) + 255) / 256)), 256, 0, st>>>(
         (const __nv_bfloat16*)qkv, cosv, sinv, (__nv_bfloat16*)q, (__nv_bfloat16*)k, (__nv_bfloat16*)v, (int)B, (int)S,
-        (int)H, (int)hd);
+        (int)H, (int)hd, bshd);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 
 int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float* cosv, const float* sinv, void* dqkv,
-                    float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, cudaStream_t st) {
+                    float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, int bshd, cudaStream_t st) {
     if (amax_reset(reinterpret_cast<uint32_t*>(amax), st)) return MOSS_ERR_CUDA;
     rope_bwd_kernel<<<dim3((unsigned)(B * S), (unsigned)((H * (hd / 8) + 255) / 256)), 256, 0, st>>>(
         (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv, cosv, sinv,
-        (__nv_bfloat16*)dqkv, reinterpret_cast<uint32_t*>(amax), (int)B, (int)S, (int)H, (int)hd);
+        (__nv_bfloat16*)dqkv, reinterpret_cast<uint32_t*>(amax), (int)B, (int)S, (int)H, (int)hd, bshd);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 

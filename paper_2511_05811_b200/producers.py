@@ -136,21 +136,32 @@ class RopeQKVFn(torch.autograd.Function):
         B, S, three_d = qkv.shape
         hd = three_d // (3 * n_heads)
         qkv = qkv if qkv.is_contiguous() else qkv.contiguous()
-        q = torch.empty(B, n_heads, S, hd, dtype=qkv.dtype, device=qkv.device)
+        # q, k, v in [B, S, H, hd] memory, returned as [B, H, S, hd] views: SDPA then
+        # leaves its output in that memory order and the O projection's input
+        # (out.transpose(1, 2).reshape(B, S, d)) is a view, not a transpose copy
+        q = torch.empty(B, S, n_heads, hd, dtype=qkv.dtype, device=qkv.device)
         k, v = torch.empty_like(q), torch.empty_like(q)
-        _lib.rope_fwd(qkv, cos, sin, q, k, v, B, S, n_heads, hd)
+        _lib.rope_fwd(qkv, cos, sin, q, k, v, B, S, n_heads, hd, bshd=True)
         ctx.save_for_backward(cos, sin)
         ctx.dims, ctx.consumer = (B, S, n_heads, hd), consumer
-        return q, k, v
+        return q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2)
 
     @staticmethod
     def backward(ctx, dq, dk, dv):
         cos, sin = ctx.saved_tensors
         B, S, H, hd = ctx.dims
-        dq, dk, dv = (t.contiguous() if t is not None else torch.zeros(B, H, S, hd, dtype=torch.bfloat16,
-                                                                        device=cos.device) for t in (dq, dk, dv))
+
+        def bshd(t):
+            # [B, H, S, hd]-shaped gradient -> [B, S, H, hd] memory (a view when SDPA
+            # produced it in that order, as it does for [B, S, H, hd]-strided inputs)
+            if t is None:
+                return torch.zeros(B, S, H, hd, dtype=torch.bfloat16, device=cos.device)
+            tt = t.transpose(1, 2)
+            return tt if tt.is_contiguous() else tt.contiguous()
+        dq, dk, dv = bshd(dq), bshd(dk), bshd(dv)
         dqkv = torch.empty(B, S, 3 * H * hd, dtype=dq.dtype, device=dq.device)
-        _lib.rope_bwd(dq, dk, dv, cos, sin, dqkv, _amax_buf(ctx.consumer, dqkv.view(B * S, -1)), B, S, H, hd)
+        _lib.rope_bwd(dq, dk, dv, cos, sin, dqkv, _amax_buf(ctx.consumer, dqkv.view(B * S, -1)), B, S, H, hd,
+                      bshd=True)
         return dqkv, None, None, None, None
 
 

@@ -77,8 +77,8 @@ def test_argument_checks_precede_launch():
     assert lib.moss_rmsnorm_bwd_workspace_bytes(4, 100) == -1
     assert lib.moss_swiglu_fwd(fake, fake, None, 4, 12, None) == 1
     assert lib.moss_swiglu_bwd(odd, fake, fake, None, 4, 16, None) == 6
-    assert lib.moss_rope_fwd(fake, fake, fake, fake, fake, fake, 1, 4, 2, 12, None) == 1
-    assert lib.moss_rope_bwd(fake, fake, fake, fake, fake, None, None, 1, 4, 2, 16, None) == 3
+    assert lib.moss_rope_fwd(fake, fake, fake, fake, fake, fake, 1, 4, 2, 12, 1, None) == 1
+    assert lib.moss_rope_bwd(fake, fake, fake, fake, fake, None, None, 1, 4, 2, 16, 1, None) == 3
     with pytest.raises(errors.InvalidShapeError):
         _lib.check(1, "x")
     with pytest.raises(errors.E8m0RangeError):

@@ -216,3 +216,28 @@ def test_glue_dy_amax_reaches_consumer():
     da = torch.randn(T, d, device="cuda", dtype=torch.bfloat16)
     a.backward(da)
     exact_amax(lin.dy_amax, da)
+
+
+def test_rope_bshd_layout_feeds_sdpa_without_copies():
+    """RopeQKVFn hands SDPA q, k, v in [B, S, H, hd] memory: SDPA's output then
+    comes back in that order, so the O projection's input is a view (no
+    transpose copy), and the SDPA gradients (same order) reach rope_bwd as views."""
+    import torch.nn.functional as F
+    B, S, H, hd = 1, 256, 8, 64
+    cfg = L.LlamaConfig(d_model=H * hd, n_heads=H, max_seq=S)
+    cos, sin = L._rope_tables(cfg, "cuda")
+    qkv = torch.randn(B, S, 3 * H * hd, device="cuda", dtype=torch.bfloat16).requires_grad_(True)
+    q, k, v = RopeQKVFn.apply(qkv, cos, sin, H, None)
+    assert q.transpose(1, 2).is_contiguous()
+    a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+    assert a.transpose(1, 2).is_contiguous(), a.stride()
+    # gradient parity against the reference rotation with [B,S,H,hd]-strided incoming grads
+    qf = qkv.detach().float().requires_grad_(True)
+    d = H * hd
+    qr, kr, vr = qf.split(d, dim=-1)
+    tr = lambda t: t.view(B, S, H, hd).transpose(1, 2)
+    q_ref, k_ref = L._apply_rope(tr(qr), cos, sin), L._apply_rope(tr(kr), cos, sin)
+    gq, gk, gv = (torch.randn(B, S, H, hd, device="cuda", dtype=torch.bfloat16).transpose(1, 2) for _ in range(3))
+    torch.autograd.backward([q, k, v], [gq, gk, gv])
+    torch.autograd.backward([q_ref, k_ref, tr(vr)], [gq.float(), gk.float(), gv.float()])
+    close_bf16(qkv.grad, qf.grad, rtol=2 ** -6, atol=1e-3)
