@@ -24,6 +24,7 @@ reference's exception classes at the step boundary.
 
 from __future__ import annotations
 
+import gc
 import math
 from typing import Callable, Iterable
 
@@ -579,14 +580,25 @@ class CudaGraphStep:
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph, stream=s):
-            # zeroing is part of the step: replays re-zero the bucket accumulators.
-            # detached loss: the captured autograd graph (and the AccumulateGrad nodes bound to
-            # this capture stream) must not outlive the capture, or a later capture of
-            # the same model on another stream picks up a cross-stream dependency
-            self.zero_grad()
-            self.loss = self._fwd_bwd()
-            self._launch(False)
+        # No Python GC during the capture: a collection there can run the destructors of
+        # stale objects (e.g. c10d Work handles of earlier eager collectives) whose CUDA
+        # calls on the legacy stream invalidate the capture.  thread_local: other threads'
+        # CUDA calls (the NCCL watchdog) do not count against this capture.
+        gc.collect()
+        gc_was_on = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.graph(self.graph, stream=s, capture_error_mode="thread_local"):
+                # zeroing is part of the step: replays re-zero the bucket accumulators.
+                # detached loss: the captured autograd graph (and the AccumulateGrad nodes bound to
+                # this capture stream) must not outlive the capture, or a later capture of
+                # the same model on another stream picks up a cross-stream dependency
+                self.zero_grad()
+                self.loss = self._fwd_bwd()
+                self._launch(False)
+        finally:
+            if gc_was_on:
+                gc.enable()
         torch.cuda.current_stream().wait_stream(s)
 
     def __call__(self, *inputs) -> torch.Tensor:
