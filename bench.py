@@ -424,7 +424,7 @@ def _max_over_ranks(v: float, dev, world: int) -> float:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    t = torch.tensor([v], device=dev if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -692,10 +692,19 @@ def main() -> None:
     import torch
     import torch.distributed as dist
 
+    # MOSS_BENCH_SHARED_GPU=1 (tests only): every rank on cuda:0 over gloo, so the N > 1
+    # code path of this script runs on a one-GPU box (NCCL refuses two ranks on one GPU)
+    shared = os.environ.get("MOSS_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
+        args.no_graph = True          # gloo collectives cannot be captured in a CUDA graph
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo", init_method="env://")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     elif args.zero1:
         dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{free_port()}", rank=0, world_size=1)
 
@@ -735,6 +744,7 @@ def main() -> None:
         dist.all_gather_object(every, me)
         comm_info = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
                      "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                     "shared_gpu_test_mode": shared,
                      "ranks": every, "distinct_devices": len({e["uuid"] for e in every})}
 
     if rank != 0:
@@ -749,10 +759,14 @@ def main() -> None:
             roof = fp8_roof(dev, local)
         except Exception as ex:  # noqa: BLE001
             roof = {"error": str(ex)[:200]}
-    have_roof = roof is not None and "sustained_tflops" in roof
-    fp8_peak = roof["sustained_tflops"] if have_roof else 2.0 * peaks.get("bf16_tflops_sustained", 1400.0)
-    peak_src = ("cuBLASLt MXFP8 8192^3 sustained, measured in this run (fp8 roof; the GEMM is timed inside the step)"
-                if have_roof else "2 x bf16_tflops_sustained of MEASURED_PEAKS.json (no fp8 roof measured)")
+    have_roof = roof is not None and "burst_tflops" in roof
+    # the BURST cuBLASLt MXFP8 figure: the in-step GEMM runs at the SM clock of a mixed
+    # memory/tensor step (see clocks), far above the ~1 GHz a seconds-long dense GEMM loop
+    # settles at under the 1 kW cap, so the sustained figure is no same-clock denominator
+    # (reported beside it as frac_of_sustained)
+    fp8_peak = roof["burst_tflops"] if have_roof else 2.0 * peaks.get("bf16_tflops", 1590.0)
+    peak_src = ("cuBLASLt MXFP8 8192^3 burst (best single launch at max clock), measured in this run"
+                if have_roof else "2 x bf16_tflops (burst) of MEASURED_PEAKS.json (no fp8 roof measured)")
     kern, ms, steps = r["kern"], r["ms"], r["steps"]
     g = kern.get("gemm", {"launches": 0, "ms": 1e-9, "work": 0})
     gemm_tflops = g["work"] / (g["ms"] / 1e3) / 1e12 if g["launches"] else 0.0
@@ -800,7 +814,7 @@ def main() -> None:
         "roofline": {"bound": "tensor", "kernel": "moss::gemm_mxf8_2cta_kernel (tcgen05.mma.cta_group::2 kind::mxf8f6f4.block_scale)",
                      "achieved": gemm_tflops, "peak": fp8_peak, "unit": "TFLOP/s", "frac": gemm_tflops / fp8_peak,
                      "peak_source": peak_src,
-                     "frac_of_burst": gemm_tflops / roof["burst_tflops"] if have_roof else None,
+                     "frac_of_sustained": gemm_tflops / roof["sustained_tflops"] if have_roof else None,
                      "frac_of_nominal_4500": gemm_tflops / 4500.0, "traffic": traffic,
                      "share_of_step": (g["ms"] / steps) / ms if g["launches"] else None,
                      "fp8_roof": roof},

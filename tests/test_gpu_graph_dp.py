@@ -63,3 +63,29 @@ def test_graphed_exchange_matches_eager(kind):
     assert graph[1] == eager[1] and graph[2] == eager[2] == 28          # s_t and rescale cadence (interval 7)
     assert (graph[3] == eager[3]).float().mean().item() > 0.99
     assert graph[0][-1] < graph[0][0]
+
+
+@pytest.mark.slow
+def test_bench_two_ranks_end_to_end():
+    """bench.py --gpus 2 spawns two ranks and runs the whole N > 1 path (bucketed
+    all-reduce DP on the layer step, the 7B-shape decoder truncated to 2 layers,
+    max-over-ranks timing, the communicator record).  On this one-GPU box the two
+    ranks share cuda:0 over gloo (MOSS_BENCH_SHARED_GPU); the driver's 8-GPU run
+    uses NCCL with the step graph-captured."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["MOSS_BENCH_SHARED_GPU"] = "1"
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3",
+                        "--layers", "2", "--llama-steps", "2", "--no-fp8-roof", "--tokens", "4096"],
+                       capture_output=True, text=True, timeout=1200, env=env, cwd=root)
+    assert p.returncode == 0, p.stderr[-3000:]
+    d = json.loads([ln for ln in p.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["n_gpus"] == 2 and d["config"]["global_batch_tokens"] == 2 * 4096
+    assert d["collectives"]["communicator"]["world_size"] == 2
+    assert d["collectives"]["allreduce_bytes"] > 0
+    assert d["llama7b"]["n_gpus"] == 2 and d["llama7b"]["tokens_per_s"] > 0
+    assert d["value"] > 0 and d["e2e"]["value"] > 0

@@ -109,6 +109,48 @@ def test_llama_125m_moss_vs_bf16_band():
     assert gap <= 0.02
 
 
+def _run_125m_against_committed_reference():
+    """The GPU run of tests/golden/make_llama125m_curve.py's RUN: same seeded
+    init (oracle.train_ref.seeded_init), same Markov data, same schedule."""
+    import os
+    import sys
+    from oracle.train_ref import seeded_init
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.join(here, "golden"))
+    from make_llama125m_curve import RUN
+    ref = np.load(os.path.join(here, "golden", "llama125m_curve.npz"))
+    cfg = L.LlamaConfig(**{**L.LLAMA_125M.__dict__, "max_seq": RUN["seq"]})
+    model = L.LlamaModel(cfg)
+    seeded_init(model, RUN["init_seed"])
+    log = train(model, L.MarkovTokens(cfg.vocab, seed=RUN["data_seed"], active=RUN["active"]), steps=RUN["steps"],
+                batch=RUN["batch"], seq=RUN["seq"], lr=RUN["lr"], warmup=RUN["warmup"], cuda_graph=True)
+    return np.asarray(log.loss), np.asarray(ref["loss"]), RUN
+
+
+C3_BAND = 0.02          # max relative gap of the 20-step smoothed curves after warm-up (SURVEY.md 8(c): <= 1-2 %)
+C3_FINAL_BAND = 0.01    # ... at the last step
+
+
+@pytest.mark.slow
+def test_llama_125m_gpu_vs_committed_cpu_reference_curve():
+    """BASELINE configs[2]: the ~125M Llama decoder, 200 synthetic-token steps,
+    GPU (MossLinear + MossAdamW, fused bf16 producers, CUDA-graph replays) vs the
+    CPU float64 reference of the same model (composed MOSS oracle linears,
+    adamw_step + autoscale, lr_at; tests/golden/make_llama125m_curve.py) from
+    the same seeded init and data: smoothed loss curves within C3_BAND."""
+    gpu, ref, run = _run_125m_against_committed_reference()
+    assert len(gpu) == len(ref) == run["steps"]
+    gpu_s = TrainLog(loss=list(gpu)).smoothed(20)
+    ref_s = TrainLog(loss=list(ref)).smoothed(20)
+    gap = np.abs(gpu_s - ref_s) / ref_s
+    w = run["warmup"]
+    print(f"125M vs CPU reference: final gpu {gpu_s[-1]:.4f} ref {ref_s[-1]:.4f}; max smoothed gap after "
+          f"warm-up {gap[w:].max():.4f} (at step {w + int(gap[w:].argmax())}), final {gap[-1]:.4f}")
+    assert ref[-1] < 0.75 * ref[0] and gpu[-1] < 0.75 * gpu[0]          # both learn
+    assert gap[w:].max() <= C3_BAND
+    assert gap[-1] <= C3_FINAL_BAND
+
+
 def test_cuda_graph_training_matches_eager():
     """CUDA-graph replays (nn.CudaGraphStep) give the same training as eager
     steps: identical data and init -> loss curves equal up to FP nondeterminism,
