@@ -545,7 +545,8 @@ def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: b
         buckets.timing = False
     kern = _lib.INSTR.summary()
     launches = _lib.INSTR.launches // steps
-    foreign = foreign_launches(step, x) if rank == 0 else None
+    # every rank runs the profiled step (it contains the gradient collectives); rank 0 reports
+    foreign = foreign_launches(step, x)
     barrier()
 
     # ---- the same timing mode at every N: CUDA-graph replays of the whole step

@@ -109,46 +109,53 @@ def test_llama_125m_moss_vs_bf16_band():
     assert gap <= 0.02
 
 
-def _run_125m_against_committed_reference():
-    """The GPU run of tests/golden/make_llama125m_curve.py's RUN: same seeded
-    init (oracle.train_ref.seeded_init), same Markov data, same schedule."""
+def _run_125m(name):
+    """The GPU run of tests/golden/make_llama125m_curve.py's RUNS[name]: same
+    seeded init (oracle.train_ref.seeded_init), same Markov data, same schedule."""
     import os
     import sys
     from oracle.train_ref import seeded_init
     here = os.path.dirname(os.path.abspath(__file__))
     sys.path.insert(0, os.path.join(here, "golden"))
-    from make_llama125m_curve import RUN
-    ref = np.load(os.path.join(here, "golden", "llama125m_curve.npz"))
-    cfg = L.LlamaConfig(**{**L.LLAMA_125M.__dict__, "max_seq": RUN["seq"]})
+    import make_llama125m_curve as M
+    run = M.RUNS[name]
+    ref = np.load(M.path(name))
+    cfg = L.LlamaConfig(**{**L.LLAMA_125M.__dict__, "max_seq": run["seq"]})
     model = L.LlamaModel(cfg)
-    seeded_init(model, RUN["init_seed"])
-    log = train(model, L.MarkovTokens(cfg.vocab, seed=RUN["data_seed"], active=RUN["active"]), steps=RUN["steps"],
-                batch=RUN["batch"], seq=RUN["seq"], lr=RUN["lr"], warmup=RUN["warmup"], cuda_graph=True)
-    return np.asarray(log.loss), np.asarray(ref["loss"]), RUN
-
-
-C3_BAND = 0.02          # max relative gap of the 20-step smoothed curves after warm-up (SURVEY.md 8(c): <= 1-2 %)
-C3_FINAL_BAND = 0.01    # ... at the last step
-
-
-@pytest.mark.slow
-def test_llama_125m_gpu_vs_committed_cpu_reference_curve():
-    """BASELINE configs[2]: the ~125M Llama decoder, 200 synthetic-token steps,
-    GPU (MossLinear + MossAdamW, fused bf16 producers, CUDA-graph replays) vs the
-    CPU float64 reference of the same model (composed MOSS oracle linears,
-    adamw_step + autoscale, lr_at; tests/golden/make_llama125m_curve.py) from
-    the same seeded init and data: smoothed loss curves within C3_BAND."""
-    gpu, ref, run = _run_125m_against_committed_reference()
+    seeded_init(model, run["init_seed"])
+    log = train(model, L.MarkovTokens(cfg.vocab, seed=run["data_seed"], active=run["active"]), steps=run["steps"],
+                batch=run["batch"], seq=run["seq"], lr=run["lr"], warmup=run["warmup"], cuda_graph=True)
+    gpu, ref = np.asarray(log.loss), np.asarray(ref["loss"])
     assert len(gpu) == len(ref) == run["steps"]
     gpu_s = TrainLog(loss=list(gpu)).smoothed(20)
     ref_s = TrainLog(loss=list(ref)).smoothed(20)
-    gap = np.abs(gpu_s - ref_s) / ref_s
+    return gpu, ref, gpu_s, ref_s, np.abs(gpu_s - ref_s) / ref_s, run
+
+
+# BASELINE configs[2]: ~125M Llama decoder, 200 steps, GPU (MossLinear + MossAdamW,
+# fused bf16 producers, CUDA-graph replays) vs the CPU float64 reference of the same
+# model (composed MOSS oracle linears, adamw_step + autoscale, lr_at), committed by
+# tests/golden/make_llama125m_curve.py.  Bands per regime (see that script):
+C3_PLATEAU_BAND = 0.01      # 20-step smoothed curves, point by point, warm-up .. step 100
+C3_CONVERGED_BAND = 0.02    # smoothed loss over the last 20 steps, after the chain is learned
+
+
+@pytest.mark.slow
+def test_llama_125m_gpu_vs_cpu_reference_descent_and_plateau():
+    gpu, ref, gpu_s, ref_s, gap, run = _run_125m("plateau")
     w = run["warmup"]
-    print(f"125M vs CPU reference: final gpu {gpu_s[-1]:.4f} ref {ref_s[-1]:.4f}; max smoothed gap after "
-          f"warm-up {gap[w:].max():.4f} (at step {w + int(gap[w:].argmax())}), final {gap[-1]:.4f}")
-    assert ref[-1] < 0.75 * ref[0] and gpu[-1] < 0.75 * gpu[0]          # both learn
-    assert gap[w:].max() <= C3_BAND
-    assert gap[-1] <= C3_FINAL_BAND
+    print(f"125M plateau run: max smoothed gap steps {w}..99 = {gap[w:100].max():.5f}; "
+          f"step 199 gpu {gpu_s[-1]:.4f} ref {ref_s[-1]:.4f}")
+    assert ref[99] < 0.75 * ref[0] and gpu[99] < 0.75 * gpu[0]          # both descend
+    assert gap[w:100].max() <= C3_PLATEAU_BAND
+
+
+@pytest.mark.slow
+def test_llama_125m_gpu_vs_cpu_reference_converged_loss():
+    gpu, ref, gpu_s, ref_s, gap, run = _run_125m("converge")
+    print(f"125M converge run: final smoothed gpu {gpu_s[-1]:.4f} ref {ref_s[-1]:.4f} gap {gap[-1]:.4f}")
+    assert ref_s[-1] < 0.3 * ref[0] and gpu_s[-1] < 0.3 * gpu[0]        # both learn the chain
+    assert gap[-1] <= C3_CONVERGED_BAND
 
 
 def test_cuda_graph_training_matches_eager():
