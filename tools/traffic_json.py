@@ -20,7 +20,7 @@ flops = 828928688128.0           # LayerStack: 3 GEMMs x 4 linears per step / 12
 tot_us = sum(l["us"] for l in launches)
 doc = {"kernel": "moss::gemm_mxf8_2cta_kernel",
        "source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum over the "
-                 f"{len(launches)} GEMM launches of one eager layer step ({src}), round 1, L2-budget raster "
+                 f"{len(launches)} GEMM launches of one eager layer step ({src}), round 2 (after the amax epilogue), L2-budget raster "
                  f"(csrc/gemm2.cu g2_raster, MOSS_GEMM2_L2MB=80); all 12 layer GEMMs incl. the MN-major dgrads",
        "dram_bytes_per_launch": sum(l["dram_read_MB"] + l["dram_write_MB"] for l in launches) / len(launches) * 1e6,
        "launches": len(launches), "algorithmic_flops_per_launch": flops,
