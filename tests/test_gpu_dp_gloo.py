@@ -36,7 +36,7 @@ def _batch(step, rank, world, tokens=512):
     return full[rank * n:(rank + 1) * n].contiguous()
 
 
-def _worker(rank, world, port, mode, q):
+def _worker(rank, world, port, mode, q, steps=4):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -51,7 +51,7 @@ def _worker(rank, world, port, mode, q):
         ex = Zero1(opt, bucket_mb=1.0) if mode == "zero1" else GradBuckets(model, bucket_mb=1.0)
         opt.grad_scale = ex.grad_scale
         losses = []
-        for step in range(4):                                    # includes a rescale at step 3
+        for step in range(steps):                                # includes a rescale at step 3
             x = _batch(step, rank, world)                        # this rank's shard of the global batch
             ex.reset()
             loss = model(x)
@@ -75,11 +75,11 @@ def _worker(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
-def _run(mode):
+def _run(mode, steps=4):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q, steps)) for r in range(2)]
     for p in procs:
         p.start()
     out = {}
@@ -108,10 +108,15 @@ def test_dp_ranks_stay_identical():
     assert np.allclose(res["allreduce"][0][3], res["zero1"][0][3], rtol=1e-3)
 
 
+DP_STEPS = 40
+DP_BAND = 0.02          # per step, relative, 2-rank mean loss vs the 1-GPU loss on the same global batch
+
+
 def test_dp_matches_single_gpu_at_same_global_batch():
-    """2 ranks x 256 tokens vs 1 process x 512 tokens, same global batches:
-    the loss curves agree within 1 % (n-GPU curve within a
-    stated band of the 1-GPU curve).  The only semantic difference is the
+    """2 ranks x 256 tokens vs 1 process x 512 tokens, same global batches, 40
+    steps (13 rescales at interval 3): the loss curves agree within DP_BAND at
+    every step (n-GPU curve within a stated band of the 1-GPU
+    curve); the loss falls by more than half over the run.  The only semantic difference is the
     per-rank activation amax; it perturbs FP8 gradients at the
     quantization-noise level, which Adam's sign-like early steps turn into
     different updates of near-zero-gradient weights, so weights are not
@@ -124,12 +129,16 @@ def test_dp_matches_single_gpu_at_same_global_batch():
     model = LayerStack(d_model=512, d_ffn=1024, device="cuda", interval=3)
     opt = MossAdamW(model, lr=1e-3)
     single = []
-    for step in range(4):
+    for step in range(DP_STEPS):
         opt.zero_grad()
         loss = model(_batch(step, 0, 1))
         loss.backward()
         opt.step()
+        opt.check()
         single.append(float(loss))
-    dp = _run("allreduce")
+    dp = _run("allreduce", steps=DP_STEPS)
     dp_loss = (np.array(dp[0][3]) + np.array(dp[1][3])) / 2          # mean of the ranks' shard losses
-    assert np.allclose(dp_loss, single, rtol=1e-2), (dp_loss, single)
+    gap = np.abs(dp_loss - np.array(single)) / np.array(single)
+    print(f"DP vs 1-GPU over {DP_STEPS} steps: max gap {gap.max():.4f}, loss {single[0]:.4f} -> {single[-1]:.4f}")
+    assert single[-1] < 0.5 * single[0]
+    assert gap.max() <= DP_BAND, gap
