@@ -449,6 +449,39 @@ def foreign_launches(step, x) -> dict | None:
         return {"error": str(ex)[:160]}
 
 
+_KINDS = (("gemm_mxf8", "gemm"), ("quant_mx2", "quant"), ("adamw_fp8", "adamw"), ("amax_kernel", "amax"),
+          ("rmsnorm", "producer"), ("swiglu", "producer"), ("rope_", "producer"), ("glue_kernel", "producer"),
+          ("sumsq", "producer"))
+
+
+def replay_kernel_times(runner, x, reps: int) -> dict | None:
+    """Per-kind kernel time of the TIMED mode itself (CUDA-graph replays), from
+    the hardware start/end timestamps CUPTI records for every kernel (torch.profiler):
+    kind -> {"ms": per step, "launches": per step}.  Unlike the event-bracketed
+    eager pass, no event record or launch latency sits inside a kernel's span."""
+    import torch
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for _ in range(reps):
+                runner(x)
+            torch.cuda.synchronize()
+        out: dict = {}
+        for ev in prof.events():
+            if ev.device_type != torch.autograd.DeviceType.CUDA or "moss::" not in ev.name:
+                continue
+            kind = next((k for pat, k in _KINDS if pat in ev.name), "other")
+            d = out.setdefault(kind, {"ms": 0.0, "launches": 0})
+            d["ms"] += ev.device_time / 1e3 / reps           # device_time: us
+            d["launches"] += 1
+        for d in out.values():
+            d["launches"] /= reps
+        return out
+    except Exception as ex:  # noqa: BLE001 - evidence only
+        return {"error": str(ex)[:160]}
+
+
 def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: bool) -> dict:
     """Build one workload, warm it up, time it; returns the measurements.
     kind: "layer" (configs[1] as a training step) or "llama7b" (configs[3]/[4])."""
@@ -577,6 +610,9 @@ def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: b
     barrier()
     ms = _max_over_ranks(s_ev.elapsed_time(e_ev) / steps, dev, world)
     opt.check("timed region")
+    # per-kernel hardware durations inside the timed mode (after the timed region)
+    replay_kern = replay_kernel_times(runner, x, min(steps, 10))
+    barrier()
 
     # ---- e2e: input from pinned host memory, loss read back every step.
     # Input pipeline as a training loop runs it: the H2D copy of step i+1's
@@ -624,7 +660,8 @@ def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: b
     # peak device memory of the training run (weights, optimizer state, FP8 copies,
     # the stashed FP8 activation codes, graph pool), before any side measurement
     peak_gb = torch.cuda.max_memory_allocated(dev) / 1e9
-    return {"ms": ms, "host_ms": host_ms, "kern": kern, "launches": launches, "foreign": foreign, "comm": comm,
+    return {"ms": ms, "host_ms": host_ms, "kern": kern, "replay_kern": replay_kern, "launches": launches,
+            "foreign": foreign, "comm": comm,
             "clocks": clocks.summary(), "e2e": e2e, "peak_gb": peak_gb, "mode": mode, "flops_step": flops_step,
             "T": T, "steps": steps}
 
@@ -639,14 +676,24 @@ def _free_cuda() -> None:
     torch.cuda.reset_peak_memory_stats()
 
 
-def _rates(kern: dict, steps: int, hbm: float):
+def _rates(kern: dict, steps: int, hbm: float, replay: dict | None = None):
+    """kind -> rates: the event-bracketed eager pass (achieved_gbs, frac_of_hbm) and,
+    when available, the CUPTI durations of the graph replays (replay_*); the
+    algorithmic work per step is the same for both."""
     def rate(kind):
         d = kern.get(kind)
         if not d or not d["launches"]:
             return None
-        return {"launches_per_step": d["launches"] // steps, "ms_per_step": d["ms"] / steps,
-                "achieved_gbs": d["work"] / (d["ms"] / 1e3) / 1e9,
-                "frac_of_hbm": d["work"] / (d["ms"] / 1e3) / 1e9 / hbm}
+        out = {"launches_per_step": d["launches"] // steps, "ms_per_step": d["ms"] / steps,
+               "achieved_gbs": d["work"] / (d["ms"] / 1e3) / 1e9,
+               "frac_of_hbm": d["work"] / (d["ms"] / 1e3) / 1e9 / hbm}
+        rp = (replay or {}).get(kind)
+        if isinstance(rp, dict) and rp.get("ms"):
+            w = d["work"] / steps
+            out.update({"replay_ms_per_step": rp["ms"], "replay_launches_per_step": rp["launches"],
+                        "replay_achieved_gbs": w / (rp["ms"] / 1e3) / 1e9,
+                        "replay_frac_of_hbm": w / (rp["ms"] / 1e3) / 1e9 / hbm})
+        return out
     return rate
 
 
@@ -661,6 +708,7 @@ def llama_summary(r: dict, world: int, args) -> dict:
             "timing_mode": r["mode"],
             "gemm_tflops_in_step": g["work"] / (g["ms"] / 1e3) / 1e12 if g["launches"] else None,
             "gemm_share_of_step": (g["ms"] / r["steps"]) / r["ms"] if g["launches"] else None,
+            "replay_kernel_ms_per_step": r.get("replay_kern"),
             "collectives": r["comm"], "clocks": r["clocks"], "peak_allocated_gb": r["peak_gb"]}
 
 
@@ -777,7 +825,10 @@ def main() -> None:
         traffic = prof.get("dram_bytes_per_launch")
     except Exception:
         pass
-    rate = _rates(kern, steps, hbm)
+    rate = _rates(kern, steps, hbm, r.get("replay_kern"))
+    rg = (r.get("replay_kern") or {}).get("gemm")
+    gemm_replay_tflops = (g["work"] / steps) / (rg["ms"] / 1e3) / 1e12 if isinstance(rg, dict) and rg.get("ms") \
+        else None
     total_kernel_ms = sum(d["ms"] for d in kern.values()) / steps
     T, flops_step = r["T"], r["flops_step"]
     e2e = None
@@ -817,6 +868,8 @@ def main() -> None:
                      "peak_source": peak_src,
                      "frac_of_sustained": gemm_tflops / roof["sustained_tflops"] if have_roof else None,
                      "frac_of_nominal_4500": gemm_tflops / 4500.0, "traffic": traffic,
+                     "achieved_replay_cupti": gemm_replay_tflops,
+                     "frac_replay_cupti": gemm_replay_tflops / fp8_peak if gemm_replay_tflops else None,
                      "share_of_step": (g["ms"] / steps) / ms if g["launches"] else None,
                      "fp8_roof": roof},
         "kernels": {"quantize": rate("quant"), "amax": rate("amax"), "adamw_fp8": rate("adamw"),
@@ -825,7 +878,10 @@ def main() -> None:
                     "host_issue_ms_per_step": r["host_ms"],
                     "timing_source": "per-kernel CUDA events from an instrumented eager pass of the same step "
                                      "(device sleep ahead of each step: no host gaps inside the events); "
-                                     "value/ms_per_step from " + r["mode"]},
+                                     "replay_*: CUPTI kernel start/end timestamps of 10 replays of the timed "
+                                     "mode after the timed region (torch.profiler); "
+                                     "value/ms_per_step from " + r["mode"],
+                    "replay_kernel_ms_per_step": r.get("replay_kern")},
         "e2e": e2e,
         "memory": {"peak_allocated_gb": r["peak_gb"],
                    "note": "torch.cuda.max_memory_allocated over warm-up, instrumented pass and timed steps"},

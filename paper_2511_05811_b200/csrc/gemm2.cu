@@ -36,7 +36,7 @@ namespace moss {
 #ifdef G2_TIMELINE
 // debug build only (tools/gemm_timeline.py): per pair, per tile, 6 globaltimer stamps
 constexpr int G2_TL_TILES = 64;
-__device__ unsigned long long g2_tl[74 * G2_TL_TILES * 6];
+__device__ unsigned long long g2_tl[74 * G2_TL_TILES * 8];
 __device__ __forceinline__ unsigned long long g2_now() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -44,7 +44,7 @@ __device__ __forceinline__ unsigned long long g2_now() {
 }
 #define G2_STAMP(pair, it, ev)                                                            \
     do {                                                                                  \
-        if ((pair) < 74 && (it) < G2_TL_TILES) g2_tl[((pair) * G2_TL_TILES + (it)) * 6 + (ev)] = g2_now(); \
+        if ((pair) < 74 && (it) < G2_TL_TILES) g2_tl[((pair) * G2_TL_TILES + (it)) * 8 + (ev)] = g2_now(); \
     } while (0)
 #else
 #define G2_STAMP(pair, it, ev) \
@@ -73,7 +73,8 @@ struct G2Layout {
     static constexpr int STG_BYTES = TMA_EPI ? 2048 : 0;       // per epilogue warp: 32 rows x 64 B
     static constexpr int OFF_STG = OFF_UNIT + SFB_BYTES;
     static constexpr int OFF_BAR = OFF_STG + EPI_WARPS * STG_BYTES;
-    static constexpr int N_BARS = 2 * STAGES + 2 * ACC;       // full, empty, tmem_full[ACC], tmem_empty[ACC]
+    // full, empty, tmem_full[ACC], tmem_empty[ACC], split[EPI_WARPS] (tail-split partial loads)
+    static constexpr int N_BARS = 2 * STAGES + 2 * ACC + EPI_WARPS;
     static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
     static constexpr int SMEM = OFF_TMEM + 16 + 1024;
     static constexpr uint32_t TMEM_COLS = 512;                 // ACC * BN = 256 accumulator + SF columns
@@ -107,6 +108,32 @@ __device__ __forceinline__ void g2_tile_coords(int tile, int m_pairs, int n_tile
     }
 }
 
+// Tail split (a 2-way stream-K of the last, partial wave; K >= 8192 only, see the
+// launcher).  Units [0, split_first)
+// are whole tiles; when the last wave holds rem <= npairs/2 tiles, each of them
+// becomes two units over the two halves of K, both in the last wave on
+// different pairs: role 1 (first half) hands its raw FP32 accumulator to role 2
+// (second half) through a global workspace + per-warp flag, role 2 adds it and
+// runs the normal epilogue.  The last wave then takes half a tile instead of a
+// whole one (M = 4096 Llama-7B GEMMs: 256 tiles on 74 pairs = 3.46 waves).
+struct G2Unit {
+    int tile, kb0, kb1, role, slot;
+};
+__device__ __forceinline__ G2Unit g2_unit(int u, int split_first, int kblocks) {
+    G2Unit w;
+    if (u < split_first) {
+        w.tile = u; w.kb0 = 0; w.kb1 = kblocks; w.role = 0; w.slot = 0;
+    } else {
+        const int v = u - split_first, h = v & 1, kh = kblocks >> 1;
+        w.slot = v >> 1;
+        w.tile = split_first + w.slot;
+        w.kb0 = h ? kh : 0;
+        w.kb1 = h ? kblocks : kh;
+        w.role = 1 + h;
+    }
+    return w;
+}
+
 // SF buffers are viewed as [bytes/256, 256] u8 tensors: one 512 B chunk = box {256, 2}
 __device__ __forceinline__ int sf_row_of_chunk(int64_t chunk) { return (int)(chunk * 2); }
 
@@ -120,7 +147,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                           const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
                           const __grid_constant__ CUtensorMap tmD, void* __restrict__ D, int64_t ldd,
                           const float* __restrict__ sA, const float* __restrict__ sB, int M, int N, int K,
-                          int unit_b, int accumulate, int raster, uint32_t* __restrict__ d_amax) {
+                          int unit_b, int accumulate, int raster, uint32_t* __restrict__ d_amax,
+                          int split_first, float4* __restrict__ sk_ws, uint32_t* __restrict__ sk_flags) {
     using L = G2Layout<STAGES, TMA_EPI, EPI_WARPS, BN>;
     constexpr int ACC = L::ACC;
     constexpr int COLS = BN / (EPI_WARPS / 4);      // accumulator columns per epilogue warp
@@ -136,6 +164,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
     uint64_t* empty = full + STAGES;
     uint64_t* tmem_full = empty + STAGES;                              // [ACC]
     uint64_t* tmem_empty = tmem_full + ACC;                            // [ACC], the leader's are live
+    uint64_t* split_bar = tmem_empty + ACC;                            // [EPI_WARPS]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -144,7 +173,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     const int m_pairs = M / (2 * G2_BM), n_tiles = N / BN, num_tiles = m_pairs * n_tiles;
     const int kblocks = K / G2_BK;
+    const int num_units = split_first + 2 * (num_tiles - split_first);
 
+    if (warp == 0 && lane == 0 && cluster_ctarank() == 0) G2_STAMP(blockIdx.x >> 1, 1, 7);   // kernel entry
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmA);
         prefetch_tmap(&tmB);
@@ -161,6 +192,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
             mbar_init(&tmem_full[a], 1);
             mbar_init(&tmem_empty[a], 2 * EPI_WARPS);
         }
+        for (int w = 0; w < EPI_WARPS; ++w) mbar_init(&split_bar[w], 1);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc_2cta(tmem_slot, L::TMEM_COLS);
@@ -183,12 +215,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
         const uint32_t cta_bytes = L::A_BYTES + L::B_BYTES + L::SFA_BYTES + (unit_b ? 0 : L::SFB_BYTES);
         int stage = 0;
         uint32_t phase = 0;
-        for (int tile = pair; tile < num_tiles; tile += npairs) {
+        for (int u = pair; u < num_units; u += npairs) {
+            const G2Unit w = g2_unit(u, split_first, kblocks);
             int mp, nt;
-            g2_tile_coords(tile, m_pairs, n_tiles, raster, mp, nt);
+            g2_tile_coords(w.tile, m_pairs, n_tiles, raster, mp, nt);
             const int mb = mp * 2 + rank;                       // this CTA's 128-row block of A
             const int n0 = nt * BN + rank * (BN / 2);           // this CTA's half of B
-            for (int kb = 0; kb < kblocks; ++kb) {
+            for (int kb = w.kb0; kb < w.kb1; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 if (elect_one()) {
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * cta_bytes);
@@ -246,7 +279,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                 }
             };
             int it_ = 0;
-            for (int tile = pair; tile < num_tiles; tile += npairs, ++it_) {
+            for (int u = pair; u < num_units; u += npairs, ++it_) {
+                const G2Unit w = g2_unit(u, split_first, kblocks);
                 // The first k-block's scale factors go into TMEM BEFORE the accumulator
                 // is released: the SF columns are separate and double-buffered, and
                 // tcgen05 ops of this thread execute in issue order, so the copy cannot
@@ -259,24 +293,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                 mbar_wait(&tmem_empty[acc], ((acc_phase >> acc) & 1u) ^ 1u);
                 tc_fence_after();
                 if (lane == 0) G2_STAMP(pair, it_, 0);
-                for (int kb = 0; kb < kblocks; ++kb) {
-                    if (kb > 0) {
+                for (int kb = w.kb0; kb < w.kb1; ++kb) {
+                    if (kb > w.kb0) {
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
                     }
                     if (elect_one()) {
                         const uint32_t sa = tm_sfa + sfbuf, sb = tm_sfb + sfbuf;
-                        if (kb > 0) copy_sf(sa, sb);
+                        if (kb > w.kb0) copy_sf(sa, sb);
                         const uint64_t adesc = adesc0 + (uint64_t)((stage * L::A_BYTES) >> 4);
                         const uint64_t bdesc = bdesc0 + (uint64_t)((stage * L::B_BYTES) >> 4);
 #pragma unroll
                         for (int k = 0; k < G2_BK / 32; ++k)
                             mma_mxf8_2cta(tmem + acc * BN, adesc + 2 * k, bdesc + (B_MN ? 256 * k : 2 * k),
-                                          idesc0 | ((uint32_t)k << 29) | ((uint32_t)k << 4), sa, sb, (kb | k) != 0);
+                                          idesc0 | ((uint32_t)k << 29) | ((uint32_t)k << 4), sa, sb,
+                                          ((kb - w.kb0) | k) != 0);
                         tc_commit_2cta_mc(&empty[stage], 0x3);
                     }
                     __syncwarp();
-                    if (kb == 0 && lane == 0) G2_STAMP(pair, it_, 1);
+                    if (kb == w.kb0 && lane == 0) G2_STAMP(pair, it_, 1);
                     sfbuf ^= SF_ALT;
                     if (++stage == STAGES) {
                         stage = 0;
@@ -305,9 +340,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
         uint32_t am = 0;
         uint32_t acc_phase = 0;
         int it_ = 0;
-        for (int tile = pair; tile < num_tiles; tile += npairs, ++it_) {
+        for (int u = pair; u < num_units; u += npairs, ++it_) {
+            const G2Unit w = g2_unit(u, split_first, kblocks);
             int mp, nt;
-            g2_tile_coords(tile, m_pairs, n_tiles, raster, mp, nt);
+            g2_tile_coords(w.tile, m_pairs, n_tiles, raster, mp, nt);
             const int row0 = (mp * 2 + rank) * G2_BM + quad * 32;
             const int col0 = nt * BN + cq * COLS;
             const int acc = ACC == 1 ? 0 : (it_ & 1);
@@ -334,6 +370,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
                              : "memory");
             if (stamp) G2_STAMP(pair, it_, 5);
             acc_phase ^= 1u << acc;
+            if (w.role) {
+                // Tail split.  A split unit is its pair's LAST unit, so once the accumulator
+                // is full every MMA has consumed its stage: the operand ring is free and
+                // each epilogue warp stages its 32 rows x COLS partial (16 KB) there.  The
+                // partial moves as ONE bulk copy per warp each way (the registers hold the
+                // accumulator; per-thread loads would run 4 deep), thread-interleaved
+                // float4s (c * 32 + lane): conflict-free smem, contiguous in global.
+                static_assert(EPI_WARPS * 32 * COLS * 4 <= STAGES * (L::A_BYTES + L::B_BYTES), "partial staging");
+                uint8_t* pst = smem + ew * (32 * COLS * 4);
+                const uint32_t pst_s = smem_u32(pst);
+                float4* part = sk_ws + ((size_t)w.slot * 2 * EPI_WARPS + rank * EPI_WARPS + ew) * (COLS / 4) * 32;
+                uint32_t* flag = sk_flags + (w.slot * 2 * EPI_WARPS + rank * EPI_WARPS + ew);
+                if (w.role == 1) {
+#pragma unroll
+                    for (int c = 0; c < COLS / 4; ++c)
+                        sts128(pst_s + (c * 32 + lane) * 16, r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        bulk_store(part, pst, 32 * COLS * 4);
+                        bulk_commit();
+                        bulk_wait0();                          // written, not just read from smem
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(1u) : "memory");
+                    }
+                    if (stamp) G2_STAMP(pair, it_, 6);
+                    continue;                                  // role 2 stores the tile
+                }
+                if (lane == 0) {
+                    uint32_t spins = 0;
+                    while (ld_acquire_gpu_u32(flag) == 0u) {
+                        if (++spins > (1u << 28)) __trap();
+                    }
+                    *flag = 0u;                                // ready for the next launch (stream-ordered)
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    mbar_arrive_expect_tx(&split_bar[ew], 32 * COLS * 4);
+                    bulk_load(pst, part, 32 * COLS * 4, &split_bar[ew]);
+                }
+                __syncwarp();
+                mbar_wait(&split_bar[ew], 0);                  // one use per launch: parity 0
+                if (stamp) G2_STAMP(pair, it_, 6);
+#pragma unroll
+                for (int c = 0; c < COLS / 4; ++c) {
+                    const uint4 q = lds128(pst_s + (c * 32 + lane) * 16);
+                    r[4 * c] = __float_as_uint(__uint_as_float(r[4 * c]) + __uint_as_float(q.x));
+                    r[4 * c + 1] = __float_as_uint(__uint_as_float(r[4 * c + 1]) + __uint_as_float(q.y));
+                    r[4 * c + 2] = __float_as_uint(__uint_as_float(r[4 * c + 2]) + __uint_as_float(q.z));
+                    r[4 * c + 3] = __float_as_uint(__uint_as_float(r[4 * c + 3]) + __uint_as_float(q.w));
+                }
+            }
             if (!TMA_EPI) {
                 const int64_t row = row0 + lane;
                 if (OUT_BF16) {
@@ -408,6 +494,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((4 + EPI_WARPS) * 32
             }
         }
         if (TMA_EPI && lane == 0) bulk_wait0();
+        if (ew == 0 && rank == 0 && lane == 0) G2_STAMP(pair, 0, 7);     // this pair's epilogue done
         if (d_amax) {
             // as f32 bits: |x| orders like its bits; NaN/Inf land at >= 0x7F800000 (flagged by the quantizer)
             uint32_t v = OUT_BF16 ? (max(am & 0xFFFFu, am >> 16) << 16) : am;
@@ -449,6 +536,46 @@ static int g2_raster(int64_t m_pairs, int64_t n_tiles, int BN, int64_t K) {
     return bytes_m <= bytes_n ? (int)gm : -(int)gn;
 }
 
+// Tail-split workspace (per device; allocated on first use outside stream
+// capture, flags zeroed once and re-zeroed by their consumers).  Split GEMMs
+// on two streams of one device at the same time would share it: every MOSS
+// GEMM of a training step runs on the compute stream.
+constexpr int G2_SK_SLOTS = 64;                   // split tiles per launch (<= npairs / 2)
+struct G2SplitWs {
+    float4* part = nullptr;
+    uint32_t* flags = nullptr;
+};
+static bool g2_split_ws(cudaStream_t st, G2SplitWs& out) {
+    static G2SplitWs ws[kMaxDevices];
+    G2SplitWs& w = ws[current_device()];
+    if (!w.part) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+        void *p = nullptr, *f = nullptr;
+        if (cudaMalloc(&p, (size_t)G2_SK_SLOTS * 256 * 256 * sizeof(float)) != cudaSuccess) return false;
+        if (cudaMalloc(&f, (size_t)G2_SK_SLOTS * 32 * sizeof(uint32_t)) != cudaSuccess ||
+            cudaMemset(f, 0, (size_t)G2_SK_SLOTS * 32 * sizeof(uint32_t)) != cudaSuccess ||
+            cudaDeviceSynchronize() != cudaSuccess) {
+            cudaFree(p);
+            return false;
+        }
+        w.part = reinterpret_cast<float4*>(p);
+        w.flags = reinterpret_cast<uint32_t*>(f);
+    }
+    out = w;
+    return true;
+}
+
+// MOSS_GEMM2_SPLIT=0 disables the tail split (A/B on the box)
+static int g2_split_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MOSS_GEMM2_SPLIT");
+        v = e ? (e[0] != '0') : 1;
+    }
+    return v;
+}
+
 template <bool OUT_BF16, int STAGES, bool TMA_EPI, int EPI_WARPS, int BN = 256, bool B_MN = false>
 static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B, const uint8_t* SFB, const float* sA,
                           const float* sB, void* D, int64_t ldd, int64_t M, int64_t N, int64_t K, int accumulate,
@@ -486,10 +613,21 @@ static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B
     const int64_t tiles = (M / (2 * G2_BM)) * (N / BN);
     const int pairs = (int)std::min<int64_t>(tiles, sm_count() / 2);
     const int raster = g2_raster(M / (2 * G2_BM), N / BN, BN, K);
+    // tail split when the last wave is at most half full (2 units per tail tile fit one wave)
+    int split_first = (int)tiles;
+    G2SplitWs sk;
+    const int64_t rem = tiles % pairs;
+    // (the partial exchange costs ~4-6 us at the end of the kernel — measured with the
+    // G2_TIMELINE build, tools/gemm_split_timeline.py — so it pays only when half a
+    // tile is longer than that: K >= 8192, a 256 x 256 x 8192 tile is ~26 us)
+    if (BN == 256 && rem > 0 && 2 * rem <= pairs && rem <= G2_SK_SLOTS && K >= 8192 &&
+        g2_split_enabled() && g2_split_ws(st, sk))
+        split_first = (int)(tiles - rem);
     if (d_amax && cudaMemsetAsync(d_amax, 0, sizeof(float), st) != cudaSuccess) return MOSS_ERR_CUDA;
     kern<<<2 * pairs, (4 + EPI_WARPS) * 32, L::SMEM, st>>>(ta, tb, tsa, tsb, td, D, ldd, sA, sB, (int)M, (int)N, (int)K,
                                                  SFB == nullptr, accumulate, raster,
-                                                 reinterpret_cast<uint32_t*>(d_amax));
+                                                 reinterpret_cast<uint32_t*>(d_amax), split_first,
+                                                 sk.part, sk.flags);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 

@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
                         const __grid_constant__ CUtensorMap tm_codes_t, int rows, int cols, float* amax_io,
                         int amax_given, uint8_t* __restrict__ sf, uint8_t* __restrict__ micro,
                         uint8_t* __restrict__ sf_t, uint8_t* __restrict__ micro_t, float* g_out, uint32_t* ws,
-                        uint32_t* flags) {
+                        uint32_t* flags, int rev) {
     extern __shared__ uint8_t q4_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(q4_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* slots = base;                                  // Q4_S x 32 KB
@@ -264,7 +264,10 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
     };
 
     // ------------------------------------------------------------ phase A: amax
-    const bool desc = !amax_given;
+    // Phase B walks DESCENDING when phase A ran (its last tiles are resident /
+    // L2-hot) and, with rev, also in producer mode: the producer kernel that
+    // just wrote x finished with its bottom rows, which are the ones still in L2.
+    const bool desc = !amax_given || rev;
     if (!amax_given) {
         if (tid == 0)
             for (int j = 0; j < min(n, Q4_S); ++j) load(j);
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
         if (tid == 0) {
             s_amax = *amax_io;
             if ((__float_as_uint(s_amax) & 0x7F800000u) == 0x7F800000u && b == 0) atomicOr(flags, MOSS_FLAG_NONFINITE);
-            for (int j = 0; j < min(n, Q4_S); ++j) load(j);
+            for (int j = 0; j < min(n, Q4_S); ++j) load(desc ? n - 1 - j : j);
         }
         __syncthreads();
     }
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
     for (int p = 0; p < n; ++p) {
         const int j = desc ? n - 1 - p : p;
         const int s = j % Q4_S;
-        if (!(desc && p < Q4_S)) wait_slot(s);     // resident tiles were waited in phase A
+        if (amax_given || p >= Q4_S) wait_slot(s);    // phase A's resident tiles were waited there
         uint8_t* Tg = slots + s * Q4_IN;               // generic: for the TMA store
         const uint32_t T = smem_u32(Tg);
         uint8_t* sfsg = sfst + (p & 1) * 1024;
@@ -447,6 +450,16 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
 }
 
 // returns false when the shape/dtype is not covered (caller falls back)
+// MOSS_Q4_REV=0 walks producer-mode tiles in ascending order (A/B on the box)
+static int q4_rev() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MOSS_Q4_REV");
+        v = e ? (e[0] != '0') : 1;
+    }
+    return v;
+}
+
 bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int amax_given, uint8_t* codes,
                      uint8_t* sf, uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t, float* g_out,
                      uint32_t* ws, uint32_t* flags, cudaStream_t st, int* status) {
@@ -499,7 +512,7 @@ bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mx, mc, mct, (int)rows, (int)cols, amax, amax_given, sf,
-                                             micro, sf_t, micro_t, g_out, ws, flags);
+                                             micro, sf_t, micro_t, g_out, ws, flags, q4_rev());
     *status = e == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
     return true;
 }

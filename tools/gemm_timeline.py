@@ -25,11 +25,11 @@ out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
 for _ in range(3):
     mx_gemm(qa.codes, qa.sf, one, qb.codes, qb.sf, one, out=out)
 torch.cuda.synchronize()
-buf = np.zeros(74 * 64 * 6, dtype=np.uint64)
+buf = np.zeros(74 * 64 * 8, dtype=np.uint64)
 lib = _lib.lib()
 lib.moss_g2_timeline.argtypes = [ctypes.c_void_p]
 assert lib.moss_g2_timeline(buf.ctypes.data) == 0
-t = buf.reshape(74, 64, 6).astype(np.int64)
+t = buf.reshape(74, 64, 8).astype(np.int64)
 tiles = (M // 256) * (N // 256)
 n_it = -(-tiles // 74)
 t0 = t[:, 0, 0].min()
