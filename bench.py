@@ -61,7 +61,8 @@ def parse():
     ap.add_argument("--workload", choices=["layer", "llama7b"], default="layer",
                     help="layer: configs[1] (default); llama7b: configs[3]/[4] Llama-2-7B-shape decoder step")
     ap.add_argument("--layers", type=int, default=32, help="llama7b: decoder layers (truncate to fit)")
-    ap.add_argument("--seq", type=int, default=4096, help="llama7b: sequence length (batch 1 per GPU)")
+    ap.add_argument("--seq", type=int, default=4096, help="llama7b: sequence length")
+    ap.add_argument("--llama-batch", type=int, default=1, help="llama7b: sequences per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-llama", action="store_true",
@@ -469,9 +470,12 @@ def replay_kernel_times(runner, x, reps: int) -> dict | None:
             torch.cuda.synchronize()
         out: dict = {}
         for ev in prof.events():
-            if ev.device_type != torch.autograd.DeviceType.CUDA or "moss::" not in ev.name:
+            if ev.device_type != torch.autograd.DeviceType.CUDA:
                 continue
-            kind = next((k for pat, k in _KINDS if pat in ev.name), "other")
+            if "moss::" not in ev.name:
+                kind = "memset/memcpy" if ev.name.startswith(("Memset", "Memcpy")) else "foreign"
+            else:
+                kind = next((k for pat, k in _KINDS if pat in ev.name), "other")
             d = out.setdefault(kind, {"ms": 0.0, "launches": 0})
             d["ms"] += ev.device_time / 1e3 / reps           # device_time: us
             d["launches"] += 1
@@ -500,9 +504,10 @@ def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: b
         cfg = LlamaConfig(**{**LLAMA2_7B.__dict__, "n_layers": args.layers, "max_seq": args.seq})
         model = LlamaModel(cfg, device=dev)
         opt = make_optimizer(model, 3e-4, 10_000, 100)
-        T = args.seq
+        B = args.llama_batch
+        T = args.seq * B
         g = torch.Generator(device=dev).manual_seed(99 + rank)      # per-rank batch shard
-        tok = torch.randint(0, cfg.vocab, (1, T + 1), device=dev, generator=g)
+        tok = torch.randint(0, cfg.vocab, (B, args.seq + 1), device=dev, generator=g)
         x, y_tok = tok[:, :-1].contiguous(), tok[:, 1:].contiguous()
         flops_step = float(cfg.gemm_flops_per_token()) * T
         fwd = lambda xin: model(xin, y_tok)
@@ -697,18 +702,29 @@ def _rates(kern: dict, steps: int, hbm: float, replay: dict | None = None):
     return rate
 
 
+def replay_gaps(r: dict) -> dict | None:
+    """Step time not covered by any kernel in the graph replays (launch gaps,
+    dependencies waiting on the front end): step ms - sum of CUPTI kernel times."""
+    rk = r.get("replay_kern")
+    if not isinstance(rk, dict) or "error" in rk:
+        return None
+    busy = sum(d["ms"] for d in rk.values() if isinstance(d, dict))
+    return {"kernel_ms_per_step": busy, "uncovered_ms_per_step": r["ms"] - busy,
+            "launches_per_step": sum(d["launches"] for d in rk.values() if isinstance(d, dict))}
+
+
 def llama_summary(r: dict, world: int, args) -> dict:
     g = r["kern"].get("gemm", {"launches": 0, "ms": 1e-9, "work": 0})
     return {"tokens_per_s": world * r["T"] / (r["ms"] / 1e3), "ms_per_step": r["ms"], "steps": r["steps"],
             "n_gpus": world, "tokens_per_gpu_per_step": r["T"],
             "config": (f"configs[3]/[4]: Llama-2-7B-shape decoder training step (d 4096, ffn 11008, 32 heads, vocab "
-                       f"32000, {args.layers} layers, seq {args.seq}, batch 1/GPU), MOSS FP8 linears, bf16 SDPA/norm/"
+                       f"32000, {args.layers} layers, seq {args.seq}, batch {args.llama_batch}/GPU), MOSS FP8 linears, bf16 SDPA/norm/"
                        f"head, MossAdamW over all params; dp{world}" +
                        (" ZeRO-1" if args.zero1 else (" bucketed NCCL all-reduce" if world > 1 else ""))),
             "timing_mode": r["mode"],
             "gemm_tflops_in_step": g["work"] / (g["ms"] / 1e3) / 1e12 if g["launches"] else None,
             "gemm_share_of_step": (g["ms"] / r["steps"]) / r["ms"] if g["launches"] else None,
-            "replay_kernel_ms_per_step": r.get("replay_kern"),
+            "replay_kernel_ms_per_step": r.get("replay_kern"), "replay_gaps": replay_gaps(r),
             "collectives": r["comm"], "clocks": r["clocks"], "peak_allocated_gb": r["peak_gb"]}
 
 
@@ -881,7 +897,7 @@ def main() -> None:
                                      "replay_*: CUPTI kernel start/end timestamps of 10 replays of the timed "
                                      "mode after the timed region (torch.profiler); "
                                      "value/ms_per_step from " + r["mode"],
-                    "replay_kernel_ms_per_step": r.get("replay_kern")},
+                    "replay_kernel_ms_per_step": r.get("replay_kern"), "replay_gaps": replay_gaps(r)},
         "e2e": e2e,
         "memory": {"peak_allocated_gb": r["peak_gb"],
                    "note": "torch.cuda.max_memory_allocated over warm-up, instrumented pass and timed steps"},
