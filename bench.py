@@ -469,9 +469,12 @@ def replay_kernel_times(runner, x, reps: int) -> dict | None:
                 runner(x)
             torch.cuda.synchronize()
         out: dict = {}
+        seq: list = []
         for ev in prof.events():
             if ev.device_type != torch.autograd.DeviceType.CUDA:
                 continue
+            if "quant_mx2" in ev.name or "gemm_mxf8" in ev.name:
+                seq.append(("q" if "quant" in ev.name else "g", round(ev.device_time, 1)))
             if "moss::" not in ev.name:
                 kind = "memset/memcpy" if ev.name.startswith(("Memset", "Memcpy")) else "foreign"
             else:
@@ -481,6 +484,8 @@ def replay_kernel_times(runner, x, reps: int) -> dict | None:
             d["launches"] += 1
         for d in out.values():
             d["launches"] /= reps
+        per = len(seq) // reps if reps else 0
+        out["last_replay_quant_gemm_us"] = seq[-per:] if per else []
         return out
     except Exception as ex:  # noqa: BLE001 - evidence only
         return {"error": str(ex)[:160]}
@@ -590,6 +595,7 @@ def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: b
     # ---- the same timing mode at every N: CUDA-graph replays of the whole step
     # (forward, backward, the captured NCCL collectives, the optimizer kernels)
     runner, mode = step, "eager steps"
+    quant_modes = None
     if not args.no_graph:
         try:
             static_x = x.detach().clone().requires_grad_(x.requires_grad)
@@ -598,6 +604,7 @@ def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: b
             for _ in range(3):          # first call is eager + capture, then replays
                 runner(x)
             mode = "CUDA-graph replays"
+            quant_modes = getattr(graphed, "capture_quant_modes", None)
         except Exception as ex:  # noqa: BLE001 - record and time eagerly rather than lose the line
             runner, mode = step, f"eager steps (graph capture failed: {str(ex)[:120]})"
         barrier()
@@ -616,7 +623,10 @@ def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: b
     ms = _max_over_ranks(s_ev.elapsed_time(e_ev) / steps, dev, world)
     opt.check("timed region")
     # per-kernel hardware durations inside the timed mode (after the timed region)
-    replay_kern = replay_kernel_times(runner, x, min(steps, 10))
+    with ClockSampler(dev.index) as rclocks:
+        replay_kern = replay_kernel_times(runner, x, min(steps, 10))
+    if isinstance(replay_kern, dict):
+        replay_kern["clocks"] = rclocks.summary()
     barrier()
 
     # ---- e2e: input from pinned host memory, loss read back every step.
@@ -666,6 +676,7 @@ def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: b
     # the stashed FP8 activation codes, graph pool), before any side measurement
     peak_gb = torch.cuda.max_memory_allocated(dev) / 1e9
     return {"ms": ms, "host_ms": host_ms, "kern": kern, "replay_kern": replay_kern, "launches": launches,
+            "quant_modes": quant_modes,
             "foreign": foreign, "comm": comm,
             "clocks": clocks.summary(), "e2e": e2e, "peak_gb": peak_gb, "mode": mode, "flops_step": flops_step,
             "T": T, "steps": steps}
@@ -708,9 +719,9 @@ def replay_gaps(r: dict) -> dict | None:
     rk = r.get("replay_kern")
     if not isinstance(rk, dict) or "error" in rk:
         return None
-    busy = sum(d["ms"] for d in rk.values() if isinstance(d, dict))
+    busy = sum(d["ms"] for d in rk.values() if isinstance(d, dict) and "ms" in d)
     return {"kernel_ms_per_step": busy, "uncovered_ms_per_step": r["ms"] - busy,
-            "launches_per_step": sum(d["launches"] for d in rk.values() if isinstance(d, dict))}
+            "launches_per_step": sum(d["launches"] for d in rk.values() if isinstance(d, dict) and "launches" in d)}
 
 
 def llama_summary(r: dict, world: int, args) -> dict:
@@ -725,6 +736,7 @@ def llama_summary(r: dict, world: int, args) -> dict:
             "gemm_tflops_in_step": g["work"] / (g["ms"] / 1e3) / 1e12 if g["launches"] else None,
             "gemm_share_of_step": (g["ms"] / r["steps"]) / r["ms"] if g["launches"] else None,
             "replay_kernel_ms_per_step": r.get("replay_kern"), "replay_gaps": replay_gaps(r),
+            "captured_quant_amax_modes": r.get("quant_modes"),
             "collectives": r["comm"], "clocks": r["clocks"], "peak_allocated_gb": r["peak_gb"]}
 
 
@@ -897,7 +909,8 @@ def main() -> None:
                                      "replay_*: CUPTI kernel start/end timestamps of 10 replays of the timed "
                                      "mode after the timed region (torch.profiler); "
                                      "value/ms_per_step from " + r["mode"],
-                    "replay_kernel_ms_per_step": r.get("replay_kern"), "replay_gaps": replay_gaps(r)},
+                    "replay_kernel_ms_per_step": r.get("replay_kern"), "replay_gaps": replay_gaps(r),
+                    "captured_quant_amax_modes": r.get("quant_modes")},
         "e2e": e2e,
         "memory": {"peak_allocated_gb": r["peak_gb"],
                    "note": "torch.cuda.max_memory_allocated over warm-up, instrumented pass and timed steps"},

@@ -69,6 +69,18 @@ def _aligned_2d(x: torch.Tensor, k: int) -> torch.Tensor:
     return x2
 
 
+# How each activation / output-gradient quantization got its tensor amax
+# (("fwd" | "bwd"), ("producer" | "in_kernel")) -> count: evidence that the
+# producer-fused amax reaches the quantizers (CudaGraphStep records the counts
+# of its captured step).
+QUANT_MODES: dict = {}
+
+
+def _count_mode(where: str, amax) -> None:
+    key = (where, "producer" if amax is not None else "in_kernel")
+    QUANT_MODES[key] = QUANT_MODES.get(key, 0) + 1
+
+
 class MossLinearFunction(torch.autograd.Function):
     """y = x W^T with MOSS FP8 forward, dgrad and wgrad (three tcgen05 GEMMs)."""
 
@@ -92,6 +104,7 @@ class MossLinearFunction(torch.autograd.Function):
         need_w = weight.requires_grad
         flags = device_flags(x.device)
         fp8_bwd = layer.fp8_backward
+        _count_mode("fwd", amax)
         op = quantize_mx2(x2d, row=True, col=need_w and fp8_bwd, flags=flags, amax=amax)
         y = mx_gemm(op.codes, op.sf, op.g, layer.w_fp8, None, layer.w_scale, out_dtype=torch.bfloat16)
         ctx.layer = layer
@@ -117,7 +130,9 @@ class MossLinearFunction(torch.autograd.Function):
             return MossLinearFunction._backward_fp(ctx, dy, layer, need_x)
         dy2d = _aligned_2d(dy, n)
         flags = device_flags(dy.device)
-        opd = quantize_mx2(dy2d, row=need_x, col=ctx.need_w, flags=flags, amax=layer.take_dy_amax(dy2d))
+        dy_amax = layer.take_dy_amax(dy2d)
+        _count_mode("bwd", dy_amax)
+        opd = quantize_mx2(dy2d, row=need_x, col=ctx.need_w, flags=flags, amax=dy_amax)
         dx = None
         if need_x:
             dx = torch.empty((dy2d.shape[0], layer.in_features), dtype=torch.bfloat16, device=dy.device)
@@ -588,6 +603,7 @@ class CudaGraphStep:
         gc_was_on = gc.isenabled()
         gc.disable()
         try:
+            before = dict(QUANT_MODES)
             with torch.cuda.graph(self.graph, stream=s, capture_error_mode="thread_local"):
                 # zeroing is part of the step: replays re-zero the bucket accumulators.
                 # detached loss: the captured autograd graph (and the AccumulateGrad nodes bound to
@@ -596,6 +612,8 @@ class CudaGraphStep:
                 self.zero_grad()
                 self.loss = self._fwd_bwd()
                 self._launch(False)
+            self.capture_quant_modes = {f"{w}/{m}": QUANT_MODES.get((w, m), 0) - before.get((w, m), 0)
+                                        for (w, m) in QUANT_MODES}
         finally:
             if gc_was_on:
                 gc.enable()

@@ -37,6 +37,7 @@ g = CudaGraphStep(fwd_bwd, opt, (x.detach().clone().requires_grad_(True),))
 for _ in range(3):
     g(x)
 torch.cuda.synchronize()
+print("captured quant amax modes:", getattr(g, "capture_quant_modes", None))
 
 
 def prof(fn, reps=5):
