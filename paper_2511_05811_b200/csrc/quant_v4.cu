@@ -220,7 +220,7 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
     return v;
 }
 
-template <bool ROW, bool COL, bool MICRO>
+template <bool ROW, bool COL, bool MICRO, bool LDSM>
 __global__ void __launch_bounds__(Q4_THREADS, 2)
     quant_mx2_v4_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_codes,
                         const __grid_constant__ CUtensorMap tm_codes_t, int rows, int cols, float* amax_io,
@@ -353,19 +353,43 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
     const uint32_t obase = (uint32_t)(rr * 128 + ((((kb0 * 2) ^ (rr & 7)) & 7) << 4));
     const int sfo_row = ((rr & 31) << 4) + ((rr >> 5) << 2) + kb0;        // + 2h
     uint32_t cbase[8];   // col-pass loads: row rb*32 + i, column 2cp -> cbase[i & 7] + i*128
-    {
+    uint32_t cob[2];     // col-pass stores: output row c, bytes cb*32 + 16j: cob[h] ^ (j << 4)
+    int sfo_col[2], ccol[2], cblk[2];
+    if (!LDSM) {
         const int c = 2 * cp;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             cbase[k] = (uint32_t)((c >> 6) * 16384 + rb * 32 * 128 + ((((c >> 3) & 7) ^ k) << 4) + ((c & 7) << 1));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) { ccol[h] = 2 * cp + h; cblk[h] = rb; }
+    } else {
+        // ldmatrix.trans column pass: the thread owns the column blocks u = 2 warp + h,
+        // each = column 8 m + l/4 (m = 2 (l%4) + (u&1) + 8 ((u>>1)&1), one of the 16
+        // 8-column groups) x rows 32 b .. 32 b + 31 (b = ((u>>2) + l%4) & 3); its 16 pair
+        // words (rows 2p, 2p+1) arrive from 4 LDSM.x4.trans, pair p = 4k + i from
+        // matrix i of load k, whose row j is addressed by lane 8i + j as row
+        // 32 b' + 8k + 2i + (j&1) of group m' (b', m' those of quad j>>1).  Conflict-free:
+        // a matrix's 8 rows sit in 16-B chunks (m'&7) ^ (2i + (j&1)), all distinct; the
+        // code stores of a quad land in distinct chunks (2b) ^ (c&7).
+        const int lane = tid & 31, warp = tid >> 5;
+        const int ai = lane >> 3, aq = (lane >> 1) & 3, as = lane & 1;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int u = 2 * warp + h;
+            const int ma = 2 * aq + (u & 1) + 8 * ((u >> 1) & 1), ba = ((u >> 2) + aq) & 3;
+            const int ra = 32 * ba + 2 * ai + as;
+            cbase[h] = (uint32_t)((ma >> 3) * 16384 + ra * 128 + (((ma & 7) ^ (ra & 7)) << 4));
+            const int qd = lane & 3;
+            const int mo = 2 * qd + (u & 1) + 8 * ((u >> 1) & 1);
+            ccol[h] = 8 * mo + (lane >> 2);
+            cblk[h] = ((u >> 2) + qd) & 3;
+        }
     }
-    uint32_t cob[2];     // col-pass stores: output row c = 2cp + h, bytes rb*32 + 16j: cob[h] ^ (j << 4)
-    int sfo_col[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        const int c = 2 * cp + h;
-        cob[h] = (uint32_t)(c * 128 + ((((rb * 2) ^ (c & 7)) & 7) << 4));
-        sfo_col[h] = 512 + ((c & 31) << 4) + ((c >> 5) << 2) + rb;
+        const int c = ccol[h];
+        cob[h] = (uint32_t)(c * 128 + ((((cblk[h] * 2) ^ (c & 7)) & 7) << 4));
+        sfo_col[h] = 512 + ((c & 31) << 4) + ((c >> 5) << 2) + cblk[h];
     }
     for (int p = 0; p < n; ++p) {
         const int j = desc ? n - 1 - p : p;
@@ -380,8 +404,17 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
 
         uint32_t ucol[32];
         if (COL) {
+            if (LDSM) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) ucol[i] = lds32(T + cbase[i & 7] + i * 128);
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        ldsm4t(T + cbase[h] + k * 1024, ucol[16 * h + 4 * k], ucol[16 * h + 4 * k + 1],
+                               ucol[16 * h + 4 * k + 2], ucol[16 * h + 4 * k + 3]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) ucol[i] = lds32(T + cbase[i & 7] + i * 128);
+            }
         }
         uint32_t rcodes[2][8];
         if (ROW) {
@@ -411,19 +444,20 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
             const uint32_t Tc = T + 16384;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                // column 2cp+h: rows i, i+1 packed as one pair word
+                // column ccol[h]: rows 2i, 2i+1 of the block packed as one pair word
                 uint32_t w[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i)
-                    w[i] = h ? __byte_perm(ucol[2 * i], ucol[2 * i + 1], 0x7632)
-                             : __byte_perm(ucol[2 * i], ucol[2 * i + 1], 0x5410);
+                    w[i] = LDSM ? ucol[16 * h + i]
+                                : (h ? __byte_perm(ucol[2 * i], ucol[2 * i + 1], 0x7632)
+                                     : __byte_perm(ucol[2 * i], ucol[2 * i + 1], 0x5410));
                 uint32_t cc[8];
                 const uint32_t code = q4_block(w, Gs, rerr, cc);
                 sts128(Tc + cob[h], cc[0], cc[1], cc[2], cc[3]);
                 sts128(Tc + (cob[h] ^ 16u), cc[4], cc[5], cc[6], cc[7]);
                 sts8(sfs + sfo_col[h], code);
                 if (MICRO && micro_t)
-                    micro_t[(int64_t)(c0 + 2 * cp + h) * (rows >> 5) + (r0 >> 5) + rb] = (uint8_t)code;
+                    micro_t[(int64_t)(c0 + ccol[h]) * (rows >> 5) + (r0 >> 5) + cblk[h]] = (uint8_t)code;
             }
         }
         fence_proxy_async_smem();
@@ -460,6 +494,16 @@ static int q4_rev() {
     return v;
 }
 
+// MOSS_Q4_LDSM=0 selects the LDS.32 + PRMT column loads (A/B on the box)
+static int q4_ldsm() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MOSS_Q4_LDSM");
+        v = e ? (e[0] != '0') : 1;
+    }
+    return v;
+}
+
 bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int amax_given, uint8_t* codes,
                      uint8_t* sf, uint8_t* micro, uint8_t* codes_t, uint8_t* sf_t, uint8_t* micro_t, float* g_out,
                      uint32_t* ws, uint32_t* flags, cudaStream_t st, int* status) {
@@ -481,13 +525,17 @@ bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int
                              CU_TENSOR_MAP_SWIZZLE_128B))
         return false;
     const bool mic = micro || micro_t;
-    using KT = decltype(&quant_mx2_v4_kernel<true, true, true>);
-    static const KT kernels[6] = {quant_mx2_v4_kernel<true, true, false>,  quant_mx2_v4_kernel<false, true, false>,
-                                  quant_mx2_v4_kernel<true, false, false>, quant_mx2_v4_kernel<true, true, true>,
-                                  quant_mx2_v4_kernel<false, true, true>,  quant_mx2_v4_kernel<true, false, true>};
-    const int ki = (row && col ? 0 : (col ? 1 : 2)) + (mic ? 3 : 0);
+    using KT = decltype(&quant_mx2_v4_kernel<true, true, true, true>);
+    static const KT kernels[12] = {
+        quant_mx2_v4_kernel<true, true, false, false>, quant_mx2_v4_kernel<false, true, false, false>,
+        quant_mx2_v4_kernel<true, false, false, false>, quant_mx2_v4_kernel<true, true, true, false>,
+        quant_mx2_v4_kernel<false, true, true, false>, quant_mx2_v4_kernel<true, false, true, false>,
+        quant_mx2_v4_kernel<true, true, false, true>, quant_mx2_v4_kernel<false, true, false, true>,
+        quant_mx2_v4_kernel<true, false, false, true>, quant_mx2_v4_kernel<true, true, true, true>,
+        quant_mx2_v4_kernel<false, true, true, true>, quant_mx2_v4_kernel<true, false, true, true>};
+    const int ki = (row && col ? 0 : (col ? 1 : 2)) + (mic ? 3 : 0) + (q4_ldsm() ? 6 : 0);
     const KT kern = kernels[ki];
-    static int occ_dev[kMaxDevices][6] = {};
+    static int occ_dev[kMaxDevices][12] = {};
     int* occ = occ_dev[current_device()];
     if (!occ[ki]) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q4_SMEM) != cudaSuccess ||
