@@ -62,7 +62,7 @@ def parse():
                     help="layer: configs[1] (default); llama7b: configs[3]/[4] Llama-2-7B-shape decoder step")
     ap.add_argument("--layers", type=int, default=32, help="llama7b: decoder layers (truncate to fit)")
     ap.add_argument("--seq", type=int, default=4096, help="llama7b: sequence length")
-    ap.add_argument("--llama-batch", type=int, default=1, help="llama7b: sequences per GPU per step")
+    ap.add_argument("--llama-batch", type=int, default=2, help="llama7b: sequences per GPU per step (2: 8192 tokens, 145 GB peak on 1 B200; profiles/r02_llama7b_batch_sweep.json)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-llama", action="store_true",

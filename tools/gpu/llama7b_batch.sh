@@ -1,6 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-for b in 2 1; do
+for b in 3 2 1; do
 timeout 900 python bench.py --workload llama7b --llama-batch $b --steps 6 --warmup 3 --no-cpu-baseline --no-e2e --no-fp8-roof > gpurun_out/b7_b$b.json 2>gpurun_out/b7_b$b.err
 python - gpurun_out/b7_b$b.json $b <<'PY'
 import json,sys
