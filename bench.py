@@ -455,18 +455,24 @@ _KINDS = (("gemm_mxf8", "gemm"), ("quant_mx2", "quant"), ("adamw_fp8", "adamw"),
           ("sumsq", "producer"))
 
 
-def replay_kernel_times(runner, x, reps: int) -> dict | None:
+def replay_kernel_times(runner, x, reps: int, sleep_cycles: int = 0) -> dict | None:
     """Per-kind kernel time of the TIMED mode itself (CUDA-graph replays), from
     the hardware start/end timestamps CUPTI records for every kernel (torch.profiler):
     kind -> {"ms": per step, "launches": per step}.  Unlike the event-bracketed
-    eager pass, no event record or launch latency sits inside a kernel's span."""
+    eager pass, no event record or launch latency sits inside a kernel's span.
+    With ``sleep_cycles`` (the eager pass) each step is preceded by a device sleep
+    and followed by a synchronize, exactly as in the event-bracketed pass."""
     import torch
     try:
         from torch.profiler import ProfilerActivity, profile
         torch.cuda.synchronize()
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
             for _ in range(reps):
+                if sleep_cycles:
+                    torch.cuda._sleep(sleep_cycles)
                 runner(x)
+                if sleep_cycles:
+                    torch.cuda.synchronize()
             torch.cuda.synchronize()
         out: dict = {}
         seq: list = []
@@ -475,6 +481,8 @@ def replay_kernel_times(runner, x, reps: int) -> dict | None:
                 continue
             if "quant_mx2" in ev.name or "gemm_mxf8" in ev.name:
                 seq.append(("q" if "quant" in ev.name else "g", round(ev.device_time, 1)))
+            if sleep_cycles and "spin_kernel" in ev.name:
+                continue                                     # the device sleep ahead of each step
             if "moss::" not in ev.name:
                 kind = "memset/memcpy" if ev.name.startswith(("Memset", "Memcpy")) else "foreign"
             else:
@@ -591,6 +599,10 @@ def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: b
     # every rank runs the profiled step (it contains the gradient collectives); rank 0 reports
     foreign = foreign_launches(step, x)
     barrier()
+    # the same eager pass with CUPTI kernel timestamps instead of events (no event
+    # record / launch latency inside a kernel's span: matters for ~30 us kernels)
+    eager_kern = replay_kernel_times(step, x, min(steps, 10 if kind == "layer" else 2), sleep_cycles=sleep_cycles)
+    barrier()
 
     # ---- the same timing mode at every N: CUDA-graph replays of the whole step
     # (forward, backward, the captured NCCL collectives, the optimizer kernels)
@@ -675,7 +687,8 @@ def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: b
     # peak device memory of the training run (weights, optimizer state, FP8 copies,
     # the stashed FP8 activation codes, graph pool), before any side measurement
     peak_gb = torch.cuda.max_memory_allocated(dev) / 1e9
-    return {"ms": ms, "host_ms": host_ms, "kern": kern, "replay_kern": replay_kern, "launches": launches,
+    return {"ms": ms, "host_ms": host_ms, "kern": kern, "replay_kern": replay_kern, "eager_kern": eager_kern,
+            "launches": launches,
             "quant_modes": quant_modes,
             "foreign": foreign, "comm": comm,
             "clocks": clocks.summary(), "e2e": e2e, "peak_gb": peak_gb, "mode": mode, "flops_step": flops_step,
@@ -692,10 +705,11 @@ def _free_cuda() -> None:
     torch.cuda.reset_peak_memory_stats()
 
 
-def _rates(kern: dict, steps: int, hbm: float, replay: dict | None = None):
-    """kind -> rates: the event-bracketed eager pass (achieved_gbs, frac_of_hbm) and,
-    when available, the CUPTI durations of the graph replays (replay_*); the
-    algorithmic work per step is the same for both."""
+def _rates(kern: dict, steps: int, hbm: float, replay: dict | None = None, eager: dict | None = None):
+    """kind -> rates: the event-bracketed eager pass (achieved_gbs, frac_of_hbm),
+    the CUPTI durations of the same eager pass (cupti_*: kernel start/end
+    timestamps, no event/launch latency) and of the graph replays (replay_*); the
+    algorithmic work per step is the same for all three."""
     def rate(kind):
         d = kern.get(kind)
         if not d or not d["launches"]:
@@ -703,12 +717,13 @@ def _rates(kern: dict, steps: int, hbm: float, replay: dict | None = None):
         out = {"launches_per_step": d["launches"] // steps, "ms_per_step": d["ms"] / steps,
                "achieved_gbs": d["work"] / (d["ms"] / 1e3) / 1e9,
                "frac_of_hbm": d["work"] / (d["ms"] / 1e3) / 1e9 / hbm}
-        rp = (replay or {}).get(kind)
-        if isinstance(rp, dict) and rp.get("ms"):
-            w = d["work"] / steps
-            out.update({"replay_ms_per_step": rp["ms"], "replay_launches_per_step": rp["launches"],
-                        "replay_achieved_gbs": w / (rp["ms"] / 1e3) / 1e9,
-                        "replay_frac_of_hbm": w / (rp["ms"] / 1e3) / 1e9 / hbm})
+        w = d["work"] / steps
+        for tag, src in (("cupti", eager), ("replay", replay)):
+            rp = (src or {}).get(kind)
+            if isinstance(rp, dict) and rp.get("ms"):
+                out.update({f"{tag}_ms_per_step": rp["ms"], f"{tag}_launches_per_step": rp["launches"],
+                            f"{tag}_achieved_gbs": w / (rp["ms"] / 1e3) / 1e9,
+                            f"{tag}_frac_of_hbm": w / (rp["ms"] / 1e3) / 1e9 / hbm})
         return out
     return rate
 
@@ -853,7 +868,7 @@ def main() -> None:
         traffic = prof.get("dram_bytes_per_launch")
     except Exception:
         pass
-    rate = _rates(kern, steps, hbm, r.get("replay_kern"))
+    rate = _rates(kern, steps, hbm, r.get("replay_kern"), r.get("eager_kern"))
     rg = (r.get("replay_kern") or {}).get("gemm")
     gemm_replay_tflops = (g["work"] / steps) / (rg["ms"] / 1e3) / 1e12 if isinstance(rg, dict) and rg.get("ms") \
         else None
@@ -906,6 +921,8 @@ def main() -> None:
                     "host_issue_ms_per_step": r["host_ms"],
                     "timing_source": "per-kernel CUDA events from an instrumented eager pass of the same step "
                                      "(device sleep ahead of each step: no host gaps inside the events); "
+                                     "cupti_*: CUPTI kernel start/end timestamps of the same eager pass "
+                                     "(kernel span only); "
                                      "replay_*: CUPTI kernel start/end timestamps of 10 replays of the timed "
                                      "mode after the timed region (torch.profiler); "
                                      "value/ms_per_step from " + r["mode"],
