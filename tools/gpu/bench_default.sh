@@ -2,7 +2,7 @@
 # one default bench line (the driver's N=1 command) + the reference arm
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv > gpurun_out/smi.txt
-/usr/bin/time -f "bench wall %e s" timeout 1200 python bench.py > gpurun_out/bench_d.log 2> gpurun_out/bench_d.err; echo "bench rc=$?" >> gpurun_out/bench_d.err
+t0=$(date +%s); timeout 1200 python bench.py > gpurun_out/bench_d.log 2> gpurun_out/bench_d.err; echo "bench rc=$? wall $(( $(date +%s) - t0 )) s" >> gpurun_out/bench_d.err
 tail -2 gpurun_out/bench_d.err
 python - <<'PY'
 import json
