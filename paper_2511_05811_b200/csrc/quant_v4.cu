@@ -40,6 +40,12 @@ constexpr int Q4_S = 3;                    // slots per CTA
 constexpr int Q4_THREADS = 256;
 constexpr int Q4_SMEM = Q4_S * Q4_IN + 2 * 1024 + 64 + 1024;   // slots, 2 x SF staging, barriers, align
 
+#ifdef Q4_TIMELINE
+// debug build only (tools/k1_timeline.py): per CTA of the LAST launch, globaltimer /
+// clock64 at entry, after the first tile arrived, at exit; SM id; tiles processed
+__device__ unsigned long long q4_tl[1024 * 8];
+#endif
+
 // workspace words (caller-owned, zero-initialised once; one stream at a time)
 constexpr int WS_ARRIVE = 0, WS_GEN = 1, WS_AMAX0 = 2;   // amax slots [2], [3] by generation parity
 
@@ -154,18 +160,43 @@ __device__ __forceinline__ uint32_t q4_scale(float bm, const Q4Global& G, bool& 
 }
 
 // Encode NP pairs of negated values at scale eff -> NP/2 code words (4 codes each, element order).
+// General path (a warp with any block outside the fast path's range lands here):
+// for any positive finite eff (normal or subnormal f32) write eff = m 2^E, m in
+// [1, 2) its significand; then x / eff = (x 2^-E) / m EXACTLY (power-of-two
+// scaling) and x 2^-E keeps x's bf16 significand while it stays normal, so the
+// 3-op division by m with r = RN(1/m) is again IEEE div.rn.f32 (the proof covers
+// every bf16 dividend significand and every f32 divisor significand; all
+// magnitudes are now O(1): |x 2^-E| <= 896, no intermediate underflows while the
+// quotient is >= 2^-103).  x 2^-E is applied as two exact power-of-two factors
+// 2^a 2^b (a, b in [-75, 75]); a product that underflows means a quotient far
+// below E4M3's 2^-10 rounding threshold: code +-0 either way, sign kept.  This
+// replaced per-element IEEE division, which made late-training gradient tensors
+// (tiny block maxima, eff < 2^-60) up to 8x slower to quantize.
 template <int NP>
 __device__ __forceinline__ void q4_encode(const float (&lo)[NP], const float (&hi)[NP], int e, float eff,
                                           const Q4Global& G, uint32_t (&out)[NP / 2]) {
-    if (G.g_normal && eff >= 0x1p-60f && eff <= 0x1p60f) {
-        // r = RN(1/eff) = RN(1/g) * 2^-e exactly (both normal)
-        const float r = __uint_as_float(__float_as_uint(G.rg) - (uint32_t)(e << 23));
-        const uint64_t nr2 = pk(-r, -r), b2 = pk(eff, eff);
+    const uint32_t eb = __float_as_uint(eff);
+    if (eb - 1u < 0x7F7FFFFFu) {                       // 0 < eff < inf
+        int E;
+        uint32_t mb;
+        if (eb >= 0x00800000u) {
+            E = (int)(eb >> 23) - 127;
+            mb = eb & 0x7FFFFFu;
+        } else {                                       // subnormal eff: normalise the significand
+            const int lz = __clz(eb) - 8;
+            E = -126 - lz;
+            mb = (eb << lz) & 0x7FFFFFu;
+        }
+        const float m = __uint_as_float(mb | 0x3F800000u);
+        const float r = __frcp_rn(m);
+        const int a = (-E) / 2, bexp = -E - a;         // 2^-E = 2^a 2^b, |a|, |b| <= 75
+        const float fa = __uint_as_float((uint32_t)(a + 127) << 23), fb = __uint_as_float((uint32_t)(bexp + 127) << 23);
+        const uint64_t nr2 = pk(-r, -r), b2 = pk(m, m), sa = pk(fa, fa), sb = pk(fb, fb);
 #pragma unroll
         for (int q = 0; q < NP / 2; ++q) {
             float a0, a1, b0, b1;
-            upk(div2n(pk(lo[2 * q], hi[2 * q]), b2, nr2), a0, a1);
-            upk(div2n(pk(lo[2 * q + 1], hi[2 * q + 1]), b2, nr2), b0, b1);
+            upk(div2n(fmul2(fmul2(pk(lo[2 * q], hi[2 * q]), sa), sb), b2, nr2), a0, a1);
+            upk(div2n(fmul2(fmul2(pk(lo[2 * q + 1], hi[2 * q + 1]), sa), sb), b2, nr2), b0, b1);
             out[q] = e4m3x4(a0, a1, b0, b1);
         }
     } else {
@@ -236,6 +267,11 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
     __shared__ float s_amax;
 
     const int tid = threadIdx.x;
+#ifdef Q4_TIMELINE
+    unsigned long long tl_t0, tl_t1 = 0, tl_c0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_t0));
+    tl_c0 = clock64();
+#endif
     const int ctiles = cols / Q4_T;
     const int ntiles = ctiles * (rows / Q4_T);
     const int G = gridDim.x, b = blockIdx.x;
@@ -395,6 +431,9 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
         const int j = desc ? n - 1 - p : p;
         const int s = j % Q4_S;
         if (amax_given || p >= Q4_S) wait_slot(s);    // phase A's resident tiles were waited there
+#ifdef Q4_TIMELINE
+        if (p == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_t1));
+#endif
         uint8_t* Tg = slots + s * Q4_IN;               // generic: for the TMA store
         const uint32_t T = smem_u32(Tg);
         uint8_t* sfsg = sfst + (p & 1) * 1024;
@@ -481,6 +520,17 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
     }
     if (tid == 0) bulk_wait0();
     if (__any_sync(0xFFFFFFFFu, rerr) && (tid & 31) == 0) atomicOr(flags, MOSS_FLAG_E8M0_RANGE);
+#ifdef Q4_TIMELINE
+    if (tid == 0 && b < 1024) {
+        unsigned long long t2;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        unsigned long long* o = q4_tl + b * 8;
+        o[0] = tl_t0; o[1] = tl_t1; o[2] = t2; o[3] = clock64() - tl_c0; o[4] = smid; o[5] = n;
+        o[6] = (unsigned long long)rows * cols; o[7] = G;
+    }
+#endif
 }
 
 // returns false when the shape/dtype is not covered (caller falls back)
@@ -566,3 +616,9 @@ bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int
 }
 
 }  // namespace moss
+
+#ifdef Q4_TIMELINE
+extern "C" int moss_q4_timeline(void* host_dst) {
+    return cudaMemcpyFromSymbol(host_dst, moss::q4_tl, sizeof(moss::q4_tl)) == cudaSuccess ? 0 : 5;
+}
+#endif

@@ -121,6 +121,32 @@ def test_quantizer_full_size_vs_c_oracle(c_oracle, cols, producer_amax):
     assert np.array_equal(host(q.codes_t), codes_t) and np.array_equal(host(q.micro_t), micro_t)
 
 
+@pytest.mark.parametrize("producer_amax", [False, True])
+def test_quantizer_tiny_gradients_vs_c_oracle(c_oracle, producer_amax):
+    """Late-training output-gradients: tensor amax ~2^-40 and block maxima spread
+    over 2^-40 .. 2^-110, so most blocks fall outside the fast path's
+    eff in [2^-60, 2^60) and take the general (scaled) path — bit-exact vs the
+    C restatement at the qkv output-gradient shape, row- and column-wise."""
+    torch.manual_seed(5)
+    x = torch.randn(M, 12288, device="cuda") * 2.0 ** -40
+    rs = torch.pow(2.0, -torch.randint(0, 70, (M, 1), device="cuda").float())        # per-row decades
+    cs = torch.pow(2.0, -torch.randint(0, 4, (1, 12288), device="cuda").float())
+    x = (x * rs * cs).to(torch.bfloat16)
+    x.view(-1)[7::4099] = -0.0
+    fl = _lib.FlagWord("cuda")
+    am = x.float().abs().max().reshape(1) if producer_amax else None
+    q = quantize_mx2(x, row=True, col=True, micro=True, flags=fl, amax=am)
+    fl.raise_if_set("quant")
+    xf = host(x.float())
+    codes, micro, gv, st = c_oracle.quant_two_level_mt(xf)
+    assert st == 0 and float(q.g.item()) == gv
+    assert int((micro < 127 - 20).sum()) > micro.size // 4          # the general path is exercised
+    assert np.array_equal(host(q.codes), codes) and np.array_equal(host(q.micro), micro)
+    codes_t, micro_t, gt, st = c_oracle.quant_two_level_mt(np.ascontiguousarray(xf.T))
+    assert st == 0 and gt == gv
+    assert np.array_equal(host(q.codes_t), codes_t) and np.array_equal(host(q.micro_t), micro_t)
+
+
 def test_dequantize_matches_reference(golden):
     """quantize.dequantize (device) == the reference's dequantize (golden_r2.npz)."""
     import os

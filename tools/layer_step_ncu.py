@@ -25,11 +25,23 @@ def step():
     return loss
 
 
+runner = step
+if "--graph" in sys.argv:        # the timed mode: one replay of the captured step
+    from paper_2511_05811_b200.nn import CudaGraphStep
+    one = torch.ones((), device=dev)
+
+    def fwd_bwd(xin):
+        loss = model(xin)
+        loss.backward(one)
+        return loss
+    xg = x.clone().requires_grad_(True)
+    g = CudaGraphStep(fwd_bwd, opt, (xg,))
+    runner = lambda: g(xg)
 for _ in range(4):
-    step()
+    runner()
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
-step()
+runner()
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 print("ok")
