@@ -714,16 +714,22 @@ def _rates(kern: dict, steps: int, hbm: float, replay: dict | None = None, eager
         d = kern.get(kind)
         if not d or not d["launches"]:
             return None
-        out = {"launches_per_step": d["launches"] // steps, "ms_per_step": d["ms"] / steps,
-               "achieved_gbs": d["work"] / (d["ms"] / 1e3) / 1e9,
-               "frac_of_hbm": d["work"] / (d["ms"] / 1e3) / 1e9 / hbm}
         w = d["work"] / steps
+        out = {"launches_per_step": d["launches"] // steps,
+               "event_ms_per_step": d["ms"] / steps,
+               "event_achieved_gbs": w / (d["ms"] / steps / 1e3) / 1e9,
+               "event_frac_of_hbm": w / (d["ms"] / steps / 1e3) / 1e9 / hbm}
         for tag, src in (("cupti", eager), ("replay", replay)):
             rp = (src or {}).get(kind)
             if isinstance(rp, dict) and rp.get("ms"):
                 out.update({f"{tag}_ms_per_step": rp["ms"], f"{tag}_launches_per_step": rp["launches"],
                             f"{tag}_achieved_gbs": w / (rp["ms"] / 1e3) / 1e9,
                             f"{tag}_frac_of_hbm": w / (rp["ms"] / 1e3) / 1e9 / hbm})
+        # headline: the kernels' own hardware spans in the instrumented eager pass (CUPTI);
+        # the event brackets add the launch latency and event processing (~2 us per launch)
+        src = "cupti" if "cupti_ms_per_step" in out else "event"
+        out.update({"ms_per_step": out[f"{src}_ms_per_step"], "achieved_gbs": out[f"{src}_achieved_gbs"],
+                    "frac_of_hbm": out[f"{src}_frac_of_hbm"], "source": src})
         return out
     return rate
 
@@ -919,10 +925,10 @@ def main() -> None:
                     "producers": rate("producer"),
                     "gemm_ms_per_step": g["ms"] / steps, "all_kernels_ms_per_step": total_kernel_ms,
                     "host_issue_ms_per_step": r["host_ms"],
-                    "timing_source": "per-kernel CUDA events from an instrumented eager pass of the same step "
-                                     "(device sleep ahead of each step: no host gaps inside the events); "
-                                     "cupti_*: CUPTI kernel start/end timestamps of the same eager pass "
-                                     "(kernel span only); "
+                    "timing_source": "quantize/adamw_fp8/producers: ms_per_step, achieved_gbs, frac_of_hbm = "
+                                     "CUPTI kernel start/end timestamps (cupti_*) of an instrumented eager pass "
+                                     "of the same step (device sleep ahead of each step); event_*: the same pass "
+                                     "with every launch bracketed by CUDA events (adds launch latency); "
                                      "replay_*: CUPTI kernel start/end timestamps of 10 replays of the timed "
                                      "mode after the timed region (torch.profiler); "
                                      "value/ms_per_step from " + r["mode"],
