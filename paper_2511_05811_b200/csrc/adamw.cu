@@ -15,6 +15,7 @@
 // Algorithmic traffic: 16 B read + 12 B written + 1 B code (+1 B transposed
 // code) per parameter with f32 grads (29 / 30 B).
 #include "common.cuh"
+#include "host_utils.cuh"
 
 namespace moss {
 
@@ -205,7 +206,7 @@ int launch_adamw(float* w, const void* g, int g_dtype, float* m, float* v, int64
                  const moss_adam_params& p, float enc_scale, const moss_adam_params* p_dev, const float* enc_dev,
                  float* scale_out, uint8_t* w_fp8, uint8_t* w_fp8_t, float* w_amax, uint32_t* nsat,
                  uint32_t* flags, cudaStream_t st) {
-    if (w_amax && cudaMemsetAsync(w_amax, 0, sizeof(float), st) != cudaSuccess) return MOSS_ERR_CUDA;
+    if (w_amax && zero_word(w_amax, st) != cudaSuccess) return MOSS_ERR_CUDA;
     if (g_dtype == MOSS_BF16)
         launch_adamw_t(w, (const __nv_bfloat16*)g, m, v, rows, cols, p, enc_scale, p_dev, enc_dev, scale_out, w_fp8,
                        w_fp8_t, w_amax, nsat, flags, st);

@@ -623,7 +623,7 @@ static int launch_gemm2_t(const uint8_t* A, const uint8_t* SFA, const uint8_t* B
     if (BN == 256 && rem > 0 && 2 * rem <= pairs && rem <= G2_SK_SLOTS && K >= 8192 &&
         g2_split_enabled() && g2_split_ws(st, sk))
         split_first = (int)(tiles - rem);
-    if (d_amax && cudaMemsetAsync(d_amax, 0, sizeof(float), st) != cudaSuccess) return MOSS_ERR_CUDA;
+    if (d_amax && zero_word(d_amax, st) != cudaSuccess) return MOSS_ERR_CUDA;
     kern<<<2 * pairs, (4 + EPI_WARPS) * 32, L::SMEM, st>>>(ta, tb, tsa, tsb, td, D, ldd, sA, sB, (int)M, (int)N, (int)K,
                                                  SFB == nullptr, accumulate, raster,
                                                  reinterpret_cast<uint32_t*>(d_amax), split_first,

@@ -1,6 +1,7 @@
 // Host-side helpers shared by the launchers: TMA tensor-map encoding through
 // the driver entry point (no -lcuda link), SM count.
 #pragma once
+#include <cstdlib>
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -69,6 +70,25 @@ inline bool smem_optin(K kern, int bytes, bool (&done)[kMaxDevices]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
     done[dev] = true;
     return true;
+}
+
+// Zero one 32-bit word on a stream.  A one-thread kernel rather than
+// cudaMemsetAsync: inside a CUDA graph a memset node between two kernel nodes
+// costs several microseconds of idle SMs on each side (kernel -> kernel
+// transitions ~0.4 us).  MOSS_MEMSET_NODE=1 restores cudaMemsetAsync (A/B).
+static __global__ void zero_word_kernel(uint32_t* p) { *p = 0u; }
+inline bool memset_nodes() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MOSS_MEMSET_NODE");
+        v = e ? (e[0] != '0') : 0;
+    }
+    return v != 0;
+}
+inline cudaError_t zero_word(void* p, cudaStream_t st) {
+    if (memset_nodes()) return cudaMemsetAsync(p, 0, 4, st);
+    zero_word_kernel<<<1, 1, 0, st>>>(reinterpret_cast<uint32_t*>(p));
+    return cudaGetLastError();
 }
 
 }  // namespace moss

@@ -1041,7 +1041,7 @@ static dim3 swiglu_grid(int64_t T, int64_t f) {
 }
 
 static int amax_reset(uint32_t* amax, cudaStream_t st) {
-    return (amax && cudaMemsetAsync(amax, 0, 4, st) != cudaSuccess) ? MOSS_ERR_CUDA : MOSS_OK;
+    return (amax && zero_word(amax, st) != cudaSuccess) ? MOSS_ERR_CUDA : MOSS_OK;
 }
 
 int launch_rmsnorm_fwd(const void* x, const void* delta, void* x_out, const float* w, float eps, void* y, float* rstd,

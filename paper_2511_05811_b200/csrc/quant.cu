@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(256) encode_scaled_kernel(const T* __restrict_
 
 // ------------------------------------------------------------------ launchers
 int launch_amax(const void* x, int dtype, int64_t n, float* amax, uint32_t* flags, cudaStream_t st) {
-    if (cudaMemsetAsync(amax, 0, sizeof(float), st) != cudaSuccess) return MOSS_ERR_CUDA;
+    if (zero_word(amax, st) != cudaSuccess) return MOSS_ERR_CUDA;
     int64_t nvec = n / 8;
     int64_t want = (nvec + 255) / 256;
     // one full wave: resident CTAs per SM x SMs (a partial second wave doubled the tail)
