@@ -62,7 +62,11 @@ def parse():
                     help="layer: configs[1] (default); llama7b: configs[3]/[4] Llama-2-7B-shape decoder step")
     ap.add_argument("--layers", type=int, default=32, help="llama7b: decoder layers (truncate to fit)")
     ap.add_argument("--seq", type=int, default=4096, help="llama7b: sequence length")
-    ap.add_argument("--llama-batch", type=int, default=2, help="llama7b: sequences per GPU per step (2: 8192 tokens, 145 GB peak on 1 B200; profiles/r02_llama7b_batch_sweep.json)")
+    ap.add_argument("--llama-batch", type=int, default=1,
+                    help="llama7b: sequences per GPU per step (configs[3]/SURVEY 8(d) C4: batch 1)")
+    ap.add_argument("--no-llama-batch2", action="store_true",
+                    help="skip the extra 7B measurement at 2 sequences per GPU (llama7b_batch2: 8192 tokens, "
+                         "145 GB peak on 1 B200; profiles/r02_llama7b_batch_sweep.json)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-llama", action="store_true",
@@ -499,7 +503,7 @@ def replay_kernel_times(runner, x, reps: int, sleep_cycles: int = 0) -> dict | N
         return {"error": str(ex)[:160]}
 
 
-def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: bool) -> dict:
+def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: bool, batch: int | None = None) -> dict:
     """Build one workload, warm it up, time it; returns the measurements.
     kind: "layer" (configs[1] as a training step) or "llama7b" (configs[3]/[4])."""
     import torch
@@ -517,7 +521,7 @@ def measure(kind: str, args, dev, rank: int, world: int, steps: int, want_e2e: b
         cfg = LlamaConfig(**{**LLAMA2_7B.__dict__, "n_layers": args.layers, "max_seq": args.seq})
         model = LlamaModel(cfg, device=dev)
         opt = make_optimizer(model, 3e-4, 10_000, 100)
-        B = args.llama_batch
+        B = batch or args.llama_batch
         T = args.seq * B
         g = torch.Generator(device=dev).manual_seed(99 + rank)      # per-rank batch shard
         tok = torch.randint(0, cfg.vocab, (B, args.seq + 1), device=dev, generator=g)
@@ -745,12 +749,12 @@ def replay_gaps(r: dict) -> dict | None:
             "launches_per_step": sum(d["launches"] for d in rk.values() if isinstance(d, dict) and "launches" in d)}
 
 
-def llama_summary(r: dict, world: int, args) -> dict:
+def llama_summary(r: dict, world: int, args, batch: int | None = None) -> dict:
     g = r["kern"].get("gemm", {"launches": 0, "ms": 1e-9, "work": 0})
     return {"tokens_per_s": world * r["T"] / (r["ms"] / 1e3), "ms_per_step": r["ms"], "steps": r["steps"],
             "n_gpus": world, "tokens_per_gpu_per_step": r["T"],
             "config": (f"configs[3]/[4]: Llama-2-7B-shape decoder training step (d 4096, ffn 11008, 32 heads, vocab "
-                       f"32000, {args.layers} layers, seq {args.seq}, batch {args.llama_batch}/GPU), MOSS FP8 linears, bf16 SDPA/norm/"
+                       f"32000, {args.layers} layers, seq {args.seq}, batch {batch or args.llama_batch}/GPU), MOSS FP8 linears, bf16 SDPA/norm/"
                        f"head, MossAdamW over all params; dp{world}" +
                        (" ZeRO-1" if args.zero1 else (" bucketed NCCL all-reduce" if world > 1 else ""))),
             "timing_mode": r["mode"],
@@ -830,6 +834,16 @@ def main() -> None:
             llama = llama_summary(rl, world, args)
         except Exception as ex:  # noqa: BLE001 - a sub-measurement must not sink the bench line
             llama = {"error": str(ex)[:300]}
+        _free_cuda()
+        barrier()
+    llama2 = None
+    if not llama_only and not args.no_llama and not args.no_llama_batch2 and args.llama_batch == 1:
+        # the same step at 2 sequences per GPU: K3's fixed 29 B/param over twice the tokens
+        try:
+            rl = measure("llama7b", args, dev, rank, world, args.llama_steps, want_e2e=False, batch=2)
+            llama2 = llama_summary(rl, world, args, batch=2)
+        except Exception as ex:  # noqa: BLE001
+            llama2 = {"error": str(ex)[:300]}
         _free_cuda()
         barrier()
 
@@ -944,6 +958,8 @@ def main() -> None:
                                        "bucket over the instrumented steps (overlaps backward)"}
     if llama is not None:
         line["llama7b"] = llama
+    if llama2 is not None:
+        line["llama7b_batch2"] = llama2
     if not llama_only:
         try:
             cmp = gemm_vs_cublas(dev, T)
