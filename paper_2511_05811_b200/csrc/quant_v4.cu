@@ -48,6 +48,7 @@ __device__ unsigned long long q4_tl[1024 * 8];
 
 // workspace words (caller-owned, zero-initialised once; one stream at a time)
 constexpr int WS_ARRIVE = 0, WS_GEN = 1, WS_AMAX0 = 2;   // amax slots [2], [3] by generation parity
+constexpr int WS_TILE = 4, WS_DONE = 5;                  // producer mode: dynamic tile counter, CTAs done
 
 __device__ __forceinline__ uint32_t q4_in_off(int r, int c) {   // bf16 tile, two 64-col SWIZZLE_128B boxes
     return (uint32_t)((c >> 6) * 16384 + r * 128 + ((((c >> 3) & 7) ^ (r & 7)) << 4) + ((c & 7) << 1));
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
                         const __grid_constant__ CUtensorMap tm_codes_t, int rows, int cols, float* amax_io,
                         int amax_given, uint8_t* __restrict__ sf, uint8_t* __restrict__ micro,
                         uint8_t* __restrict__ sf_t, uint8_t* __restrict__ micro_t, float* g_out, uint32_t* ws,
-                        uint32_t* flags, int rev) {
+                        uint32_t* flags, int rev, int dyn) {
     extern __shared__ uint8_t q4_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(q4_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* slots = base;                                  // Q4_S x 32 KB
@@ -265,10 +266,12 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
     uint64_t* full = reinterpret_cast<uint64_t*>(sfst + 2048);
     __shared__ uint32_t red[Q4_THREADS / 32];
     __shared__ float s_amax;
+    __shared__ int slot_tile[Q4_S];
 
     const int tid = threadIdx.x;
 #ifdef Q4_TIMELINE
     unsigned long long tl_t0, tl_t1 = 0, tl_c0;
+    int tl_tiles = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_t0));
     tl_c0 = clock64();
 #endif
@@ -293,6 +296,43 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
         tma_load_2d(slots + s * Q4_IN, &tm_x, &full[s], c0, r0);
         tma_load_2d(slots + s * Q4_IN + 16384, &tm_x, &full[s], c0 + 64, r0);
     };
+    const bool desc = !amax_given || rev;
+    // Producer mode, dynamic schedule (dyn): CTAs take tiles from a global counter in
+    // the workspace (atomicAdd by the loading thread, tile index handed to the
+    // consumers through slot_tile[] before the barrier arrive), so the CTAs finish
+    // together — a static round-robin left a ~25 % tail of idle SMs (per-CTA exit
+    // times 80..107 us on a 107 us launch, -DQ4_TIMELINE).  Ordinal k is tile k
+    // (ascending) or ntiles-1-k (desc: the producer's last rows are L2-hot).
+    // The last CTA to finish resets the counter: no memset, graph-capturable.
+    // Hybrid: the first P positions of every CTA are static (ordinal p*G + b: no
+    // atomic in the pipeline ramp), the rest come from the counter (ordinal
+    // P*G + c), about the last quarter of the tensor — the part where a static
+    // schedule's imbalance shows.  The counter is fetched one load ahead
+    // (c_next), so the atomic's round trip overlaps a tile instead of delaying
+    // the next TMA issue.
+    const int P_static = max(Q4_S, (ntiles * 3 / 4) / G);
+    int c_next = (dyn && tid == 0) ? (int)atomicAdd(&ws[WS_TILE], 1u) : 0;
+    int pos = 0;   // next position to load (loading thread only)
+    auto load_dyn = [&](int s) {   // one thread
+        int k;
+        if (pos < P_static) {
+            k = pos * G + b;
+        } else {
+            k = P_static * G + c_next;
+            if (k < ntiles) c_next = (int)atomicAdd(&ws[WS_TILE], 1u);
+        }
+        ++pos;
+        const int tile = k < ntiles ? (desc ? ntiles - 1 - k : k) : -1;
+        slot_tile[s] = tile;
+        if (tile < 0) {
+            mbar_arrive(&full[s]);
+            return;
+        }
+        const int r0 = (tile / ctiles) * Q4_T, c0 = (tile % ctiles) * Q4_T;
+        mbar_arrive_expect_tx(&full[s], Q4_IN);
+        tma_load_2d(slots + s * Q4_IN, &tm_x, &full[s], c0, r0);
+        tma_load_2d(slots + s * Q4_IN + 16384, &tm_x, &full[s], c0 + 64, r0);
+    };
     uint32_t par = 0;   // bit s: parity of the next completion of slot s
     auto wait_slot = [&](int s) {
         mbar_wait(&full[s], (par >> s) & 1u);
@@ -303,7 +343,6 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
     // Phase B walks DESCENDING when phase A ran (its last tiles are resident /
     // L2-hot) and, with rev, also in producer mode: the producer kernel that
     // just wrote x finished with its bottom rows, which are the ones still in L2.
-    const bool desc = !amax_given || rev;
     if (!amax_given) {
         if (tid == 0)
             for (int j = 0; j < min(n, Q4_S); ++j) load(j);
@@ -365,7 +404,10 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
         if (tid == 0) {
             s_amax = *amax_io;
             if ((__float_as_uint(s_amax) & 0x7F800000u) == 0x7F800000u && b == 0) atomicOr(flags, MOSS_FLAG_NONFINITE);
-            for (int j = 0; j < min(n, Q4_S); ++j) load(desc ? n - 1 - j : j);
+            if (dyn)
+                for (int s = 0; s < Q4_S; ++s) load_dyn(s);
+            else
+                for (int j = 0; j < min(n, Q4_S); ++j) load(desc ? n - 1 - j : j);
         }
         __syncthreads();
     }
@@ -427,10 +469,15 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
         cob[h] = (uint32_t)(c * 128 + ((((cblk[h] * 2) ^ (c & 7)) & 7) << 4));
         sfo_col[h] = 512 + ((c & 31) << 4) + ((c >> 5) << 2) + cblk[h];
     }
-    for (int p = 0; p < n; ++p) {
+    for (int p = 0; dyn || p < n; ++p) {
         const int j = desc ? n - 1 - p : p;
-        const int s = j % Q4_S;
+        const int s = dyn ? p % Q4_S : j % Q4_S;
         if (amax_given || p >= Q4_S) wait_slot(s);    // phase A's resident tiles were waited there
+        const int tile = dyn ? slot_tile[s] : b + j * G;
+        if (tile < 0) break;                           // dyn: the counter ran out (CTA-uniform)
+#ifdef Q4_TIMELINE
+        tl_tiles = p + 1;
+#endif
 #ifdef Q4_TIMELINE
         if (p == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_t1));
 #endif
@@ -438,7 +485,6 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
         const uint32_t T = smem_u32(Tg);
         uint8_t* sfsg = sfst + (p & 1) * 1024;
         const uint32_t sfs = smem_u32(sfsg);
-        const int tile = b + j * G;
         const int r0 = (tile / ctiles) * Q4_T, c0 = (tile % ctiles) * Q4_T;
 
         uint32_t ucol[32];
@@ -514,11 +560,24 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
             // the store of position p-1 has read its slot and SF staging -> refill the slot with p+2
             if (p >= 1) {
                 asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                if (p + 2 < n) load(desc ? n - 1 - (p + 2) : p + 2);
+                if (dyn)
+                    load_dyn((p + 2) % Q4_S);
+                else if (p + 2 < n)
+                    load(desc ? n - 1 - (p + 2) : p + 2);
             }
         }
     }
-    if (tid == 0) bulk_wait0();
+    if (tid == 0) {
+        bulk_wait0();
+        if (dyn) {
+            // every fetch of this CTA precedes its arrival here; the last CTA resets
+            __threadfence();
+            if (atomicAdd(&ws[WS_DONE], 1u) == (uint32_t)G - 1) {
+                ws[WS_TILE] = 0;
+                ws[WS_DONE] = 0;
+            }
+        }
+    }
     if (__any_sync(0xFFFFFFFFu, rerr) && (tid & 31) == 0) atomicOr(flags, MOSS_FLAG_E8M0_RANGE);
 #ifdef Q4_TIMELINE
     if (tid == 0 && b < 1024) {
@@ -527,7 +586,7 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
         uint32_t smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         unsigned long long* o = q4_tl + b * 8;
-        o[0] = tl_t0; o[1] = tl_t1; o[2] = t2; o[3] = clock64() - tl_c0; o[4] = smid; o[5] = n;
+        o[0] = tl_t0; o[1] = tl_t1; o[2] = t2; o[3] = clock64() - tl_c0; o[4] = smid; o[5] = tl_tiles;
         o[6] = (unsigned long long)rows * cols; o[7] = G;
     }
 #endif
@@ -542,6 +601,13 @@ static int q4_rev() {
         v = e ? (e[0] != '0') : 1;
     }
     return v;
+}
+
+// MOSS_Q4_DYN=0: static round-robin tiles in producer mode (read at every launch:
+// A/B inside one process, e.g. two graphs captured under each setting)
+static int q4_dyn() {
+    const char* e = getenv("MOSS_Q4_DYN");
+    return e ? (e[0] != '0') : 1;
 }
 
 // MOSS_Q4_LDSM=0 selects the LDS.32 + PRMT column loads (A/B on the box)
@@ -584,6 +650,7 @@ bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int
         quant_mx2_v4_kernel<true, false, false, true>, quant_mx2_v4_kernel<true, true, true, true>,
         quant_mx2_v4_kernel<false, true, true, true>, quant_mx2_v4_kernel<true, false, true, true>};
     const int ki = (row && col ? 0 : (col ? 1 : 2)) + (mic ? 3 : 0) + (q4_ldsm() ? 6 : 0);
+
     const KT kern = kernels[ki];
     static int occ_dev[kMaxDevices][12] = {};
     int* occ = occ_dev[current_device()];
@@ -598,6 +665,10 @@ bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int
     }
     const int64_t ntiles = (rows / Q4_T) * (cols / Q4_T);
     const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * occ[ki]);
+    // dynamic tail only for big tensors (>= 8 tiles per CTA): standalone 8192 x {11008, 12288,
+    // 22016} +6-9 %; at <= 7 tiles per CTA the counter's atomics cost more than the tail
+    // (4096^2: 22.5 vs 20.5 us); in the layer step's graph the two schedules measured equal
+    const int dyn = amax_given && ws && q4_dyn() && ntiles >= 8 * (int64_t)grid;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(Q4_THREADS);
@@ -610,7 +681,7 @@ bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mx, mc, mct, (int)rows, (int)cols, amax, amax_given, sf,
-                                             micro, sf_t, micro_t, g_out, ws, flags, q4_rev());
+                                             micro, sf_t, micro_t, g_out, ws, flags, q4_rev(), dyn);
     *status = e == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
     return true;
 }

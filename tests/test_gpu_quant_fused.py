@@ -130,3 +130,36 @@ def test_fused_in_cuda_graph(monkeypatch):
         for name in ("codes", "sf", "codes_t", "sf_t", "g"):
             assert torch.equal(getattr(op, name), getattr(ref, name)), (i, name)
     raise_if_flagged("cuda", "graph")
+
+
+def test_producer_mode_dynamic_schedule(monkeypatch):
+    """Producer mode on a big tensor (>= 8 tiles per CTA) takes the tail of its tiles
+    from a global counter in the workspace, reset by the last CTA: outputs equal the
+    static schedule (MOSS_Q4_DYN=0) bit for bit, across back-to-back launches and
+    CUDA-graph replays (the counter must come back to 0 every launch)."""
+    monkeypatch.setattr(Q, "FUSED", True)
+    torch.manual_seed(3)
+    x = torch.randn(8192, 11008, device="cuda", dtype=torch.bfloat16)
+    x.view(-1)[::4093] *= 60.0
+    am = x.float().abs().max().reshape(1)
+    monkeypatch.setenv("MOSS_Q4_DYN", "0")
+    ref = Q.quantize_mx2(x, row=True, col=True, micro=True, amax=am)
+    monkeypatch.setenv("MOSS_Q4_DYN", "1")
+    for _ in range(3):
+        got = Q.quantize_mx2(x, row=True, col=True, micro=True, amax=am)
+        for name in ("codes", "sf", "micro", "codes_t", "sf_t", "micro_t", "g"):
+            assert torch.equal(getattr(ref, name), getattr(got, name)), name
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        Q.quantize_mx2(x, row=True, col=True, amax=am)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        op = Q.quantize_mx2(x, row=True, col=True, amax=am)
+    for _ in range(4):
+        g.replay()
+        torch.cuda.synchronize()
+        for name in ("codes", "sf", "codes_t", "sf_t", "g"):
+            assert torch.equal(getattr(op, name), getattr(ref, name)), name
+    raise_if_flagged("cuda", "dyn")
