@@ -603,11 +603,12 @@ static int q4_rev() {
     return v;
 }
 
-// MOSS_Q4_DYN=0: static round-robin tiles in producer mode (read at every launch:
-// A/B inside one process, e.g. two graphs captured under each setting)
+// MOSS_Q4_DYN=0: static round-robin tiles in producer mode; =2: the dynamic tail at
+// every size (tests, sanitizers).  Read at every launch: A/B inside one process,
+// e.g. two graphs captured under each setting.
 static int q4_dyn() {
     const char* e = getenv("MOSS_Q4_DYN");
-    return e ? (e[0] != '0') : 1;
+    return e ? (e[0] == '2' ? 2 : e[0] != '0') : 1;
 }
 
 // MOSS_Q4_LDSM=0 selects the LDS.32 + PRMT column loads (A/B on the box)
@@ -668,7 +669,8 @@ bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int
     // dynamic tail only for big tensors (>= 8 tiles per CTA): standalone 8192 x {11008, 12288,
     // 22016} +6-9 %; at <= 7 tiles per CTA the counter's atomics cost more than the tail
     // (4096^2: 22.5 vs 20.5 us); in the layer step's graph the two schedules measured equal
-    const int dyn = amax_given && ws && q4_dyn() && ntiles >= 8 * (int64_t)grid;
+    const int dm = q4_dyn();
+    const int dyn = amax_given && ws && dm && (dm == 2 || ntiles >= 8 * (int64_t)grid);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(Q4_THREADS);

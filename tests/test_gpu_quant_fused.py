@@ -163,3 +163,20 @@ def test_producer_mode_dynamic_schedule(monkeypatch):
         for name in ("codes", "sf", "codes_t", "sf_t", "g"):
             assert torch.equal(getattr(op, name), getattr(ref, name)), name
     raise_if_flagged("cuda", "dyn")
+
+
+@pytest.mark.parametrize("shape", [(128, 128), (384, 640), (2048, 4096)])
+def test_producer_mode_dynamic_schedule_forced(shape, monkeypatch):
+    """MOSS_Q4_DYN=2 forces the counter-fed tail at any size (more CTAs than tiles,
+    one tile per CTA, ragged last wave): same bytes as the static schedule."""
+    monkeypatch.setattr(Q, "FUSED", True)
+    torch.manual_seed(shape[1])
+    x = torch.randn(shape, device="cuda", dtype=torch.bfloat16)
+    am = x.float().abs().max().reshape(1)
+    monkeypatch.setenv("MOSS_Q4_DYN", "0")
+    ref = Q.quantize_mx2(x, row=True, col=True, micro=True, amax=am)
+    monkeypatch.setenv("MOSS_Q4_DYN", "2")
+    for _ in range(3):
+        got = Q.quantize_mx2(x, row=True, col=True, micro=True, amax=am)
+        for name in ("codes", "sf", "micro", "codes_t", "sf_t", "micro_t", "g"):
+            assert torch.equal(getattr(ref, name), getattr(got, name)), name

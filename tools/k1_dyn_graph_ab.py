@@ -35,6 +35,7 @@ for v in ("1", "0"):
     graphs[v] = g
 k1 = {v: [] for v in graphs}
 step = {v: [] for v in graphs}
+busy = {v: [] for v in graphs}
 for blk in range(int(sys.argv[1]) if len(sys.argv) > 1 else 6):
     for v, g in graphs.items():
         for _ in range(10):
@@ -48,8 +49,22 @@ for blk in range(int(sys.argv[1]) if len(sys.argv) > 1 else 6):
             e.record()
             torch.cuda.synchronize()
         q = [ev.device_time for ev in prof.events() if "quant_mx2" in ev.name]
+        kev = sorted((ev.time_range.start, ev.time_range.end) for ev in prof.events()
+                     if ev.device_type == torch.autograd.DeviceType.CUDA)
+        span = kev[-1][1] - kev[0][0]
+        covered, cur_s, cur_e = 0.0, None, None        # union of kernel intervals
+        for a, b in kev:
+            if cur_e is None or a > cur_e:
+                if cur_e is not None:
+                    covered += cur_e - cur_s
+                cur_s, cur_e = a, b
+            else:
+                cur_e = max(cur_e, b)
+        covered += cur_e - cur_s
+        busy[v].append((span - covered) / 5)
         k1[v].append(np.array(q).reshape(5, -1).mean(0))
         step[v].append(s.elapsed_time(e) / 5)
 for v in graphs:
     a = np.median(np.stack(k1[v]), 0)
-    print(f"DYN={v}: step {np.median(step[v]):.3f} ms; K1 us per launch {np.round(a, 1).tolist()} sum {a.sum():.1f}")
+    print(f"DYN={v}: step {np.median(step[v]):.3f} ms; idle between kernels {np.median(busy[v]):.1f} us/step; "
+          f"K1 us per launch {np.round(a, 1).tolist()} sum {a.sum():.1f}")

@@ -28,6 +28,13 @@ if "k1" in which:
         am = x.float().abs().max().reshape(1)
         q2 = quantize_mx2(x, row=True, col=True, flags=fl, amax=am)             # producer-amax mode
         torch.cuda.synchronize()
+        os.environ["MOSS_Q4_DYN"] = "2"                                          # dynamic tile tail
+        q3 = quantize_mx2(x, row=True, col=True, flags=fl, amax=am)
+        q3 = quantize_mx2(x, row=True, col=True, flags=fl, amax=am)             # counter reset
+        os.environ.pop("MOSS_Q4_DYN")
+        xt = (x.float() * torch.pow(2.0, -torch.randint(40, 110, (rows, 1), device=dev).float())).to(torch.bfloat16)
+        q4 = quantize_mx2(xt, row=True, col=True, flags=fl)                      # general (scaled) path
+        torch.cuda.synchronize()
         assert torch.equal(q.codes, q2.codes) and torch.equal(q.codes_t, q2.codes_t)
     print("k1 ok", flush=True)
 if "k2" in which:
