@@ -86,6 +86,9 @@ int moss_quant_mx2(const void* x, int dtype, int64_t rows, int64_t cols, const f
  *                skips the reduction and the barrier)
  *   workspace    moss_workspace_bytes() bytes of device memory, zeroed once
  *                by the caller and reused; one stream at a time per workspace
+ *                (grid-barrier words of the in-kernel amax; in producer mode the
+ *                tile counter of the load-balanced tail; both reset by the
+ *                kernel's last CTA, so the words are zero between launches)
  *   other arguments as moss_quant_mx2.
  * bf16 tensors with rows % 128 == 0 and cols % 128 == 0 take the fused
  * kernel; other shapes/dtypes run moss_amax + moss_quant_mx2 internally. */
