@@ -88,4 +88,5 @@ def test_bench_two_ranks_end_to_end():
     assert d["collectives"]["communicator"]["world_size"] == 2
     assert d["collectives"]["allreduce_bytes"] > 0
     assert d["llama7b"]["n_gpus"] == 2 and d["llama7b"]["tokens_per_s"] > 0
+    assert d["llama7b_batch2"]["n_gpus"] == 2 and d["llama7b_batch2"]["tokens_per_gpu_per_step"] == 2 * 4096
     assert d["value"] > 0 and d["e2e"]["value"] > 0
