@@ -1,7 +1,9 @@
-"""A/B of K1's producer-mode tile schedule inside the layer step's CUDA graph, one
-process: graph A captured with MOSS_Q4_DYN=1 (dynamic tile counter), graph B with
-MOSS_Q4_DYN=0 (static round-robin); replays alternate in blocks, CUPTI durations
-of the 8 K1 launches per step (medians over the blocks), plus the step time."""
+"""A/B of a launch-time switch inside the layer step's CUDA graph, one process:
+one graph captured per setting of an environment variable read at launch time
+(default MOSS_Q4_DYN=1,0: K1's dynamic vs static tile schedule; e.g.
+`python tools/k1_dyn_graph_ab.py 8 MOSS_PDL=0,1`); replays alternate in blocks,
+CUPTI durations of the 8 K1 launches per step (medians over the blocks), the
+step time and the idle time between kernels."""
 import os
 import sys
 
@@ -26,9 +28,10 @@ def fwd_bwd(xin):
     return loss
 
 
+VAR, VALS = (sys.argv[2].split("=") if len(sys.argv) > 2 else ("MOSS_Q4_DYN", "1,0"))
 graphs = {}
-for v in ("1", "0"):
-    os.environ["MOSS_Q4_DYN"] = v
+for v in VALS.split(","):
+    os.environ[VAR] = v
     g = CudaGraphStep(fwd_bwd, opt, (x.detach().clone().requires_grad_(True),))
     g(x)
     g(x)
@@ -66,5 +69,5 @@ for blk in range(int(sys.argv[1]) if len(sys.argv) > 1 else 6):
         step[v].append(s.elapsed_time(e) / 5)
 for v in graphs:
     a = np.median(np.stack(k1[v]), 0)
-    print(f"DYN={v}: step {np.median(step[v]):.3f} ms; idle between kernels {np.median(busy[v]):.1f} us/step; "
+    print(f"{VAR}={v}: step {np.median(step[v]):.3f} ms; idle between kernels {np.median(busy[v]):.1f} us/step; "
           f"K1 us per launch {np.round(a, 1).tolist()} sum {a.sum():.1f}")
