@@ -177,3 +177,35 @@ def test_cuda_graph_training_matches_eager():
     assert states[True][0] == states[False][0] and states[True][1] == states[False][1] == 28
     agree = (states[True][2] == states[False][2]).float().mean().item()
     assert agree > 0.99
+
+
+@pytest.mark.slow
+def test_llama7b_shape_band_deconfounded():
+    """configs[3] semantics at the Llama-2-7B layer shape (d 4096, ffn 11008, 32 heads,
+    vocab 32000, seq 4096; 8 of the 32 layers to keep the test short — the full-depth
+    run is profiles/r02_llama7b_band_deconfounded.txt, tools/band_7b_v2.py): pairs that
+    differ in ONE thing, same init, data and CUDA-graph stepping.  MOSS FP8 linears vs
+    bf16 linears (torch glue both), and our fused producers vs torch glue (MOSS both).
+    Bands: final smoothed loss within 1 %, second half of the run within 2 % (the steep
+    descent right after warm-up shifts by a step or two and is not compared)."""
+    import gc
+    steps, warm = 150, 15
+    runs = {"moss_fused": dict(moss=True, fused_ops=True), "moss_torchglue": dict(moss=True, fused_ops=False),
+            "bf16_torchglue": dict(moss=False, fused_ops=False)}
+    res = {}
+    for name, kw in runs.items():
+        torch.manual_seed(0)
+        cfg = L.LlamaConfig(**{**L.LLAMA2_7B.__dict__, "n_layers": 8, "max_seq": 4096, **kw})
+        model = L.LlamaModel(cfg)
+        log = train(model, L.MarkovTokens(cfg.vocab, seed=1, active=128), steps=steps, batch=1, seq=4096, lr=3e-4,
+                    warmup=warm, cuda_graph=True)
+        res[name] = log.smoothed(25)
+        assert res[name][-1] < 0.15 * log.loss[0]                      # every run learns the chain
+        del model, log
+        gc.collect()
+        torch.cuda.empty_cache()
+    for a, b in (("moss_torchglue", "bf16_torchglue"), ("moss_fused", "moss_torchglue")):
+        gap = np.abs(res[a] - res[b]) / res[b]
+        print(f"7B shape x8: {a} vs {b}: final {gap[-1]:.4f}, second half max {gap[steps // 2:].max():.4f}")
+        assert gap[-1] <= 0.01
+        assert gap[steps // 2:].max() <= 0.02
