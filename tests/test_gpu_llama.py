@@ -138,6 +138,10 @@ def _run_125m(name):
 # tests/golden/make_llama125m_curve.py.  Bands per regime (see that script):
 C3_PLATEAU_BAND = 0.01      # 20-step smoothed curves, point by point, warm-up .. step 100
 C3_CONVERGED_BAND = 0.02    # smoothed loss over the last 20 steps, after the chain is learned
+# converge run, point by point: the first descent (warm-up .. step 44) within 1 % (measured 0.03 %); the
+# second drop (steps ~45-100) runs a few steps ahead on the GPU (max 9 % at step 67 — a timing shift, the
+# curves meet again: tools/c3_converge_gap.py), so it is not compared; from step 100 within 2 % (1.5 %)
+C3_DESCENT_BAND = 0.01
 
 
 @pytest.mark.slow
@@ -153,9 +157,13 @@ def test_llama_125m_gpu_vs_cpu_reference_descent_and_plateau():
 @pytest.mark.slow
 def test_llama_125m_gpu_vs_cpu_reference_converged_loss():
     gpu, ref, gpu_s, ref_s, gap, run = _run_125m("converge")
-    print(f"125M converge run: final smoothed gpu {gpu_s[-1]:.4f} ref {ref_s[-1]:.4f} gap {gap[-1]:.4f}")
+    w = run["warmup"]
+    print(f"125M converge run: final smoothed gpu {gpu_s[-1]:.4f} ref {ref_s[-1]:.4f} gap {gap[-1]:.4f}; "
+          f"max smoothed gap steps {w}..44 = {gap[w:45].max():.4f}, steps 100.. = {gap[100:].max():.4f}")
     assert ref_s[-1] < 0.3 * ref[0] and gpu_s[-1] < 0.3 * gpu[0]        # both learn the chain
     assert gap[-1] <= C3_CONVERGED_BAND
+    assert gap[w:45].max() <= C3_DESCENT_BAND           # first descent, point by point
+    assert gap[100:].max() <= C3_CONVERGED_BAND         # after the second drop, point by point
 
 
 def test_cuda_graph_training_matches_eager():
