@@ -12,9 +12,11 @@
 //            every CTA then reads the tensor amax (g = amax/448).
 //   phase B  quantize the resident tiles first, then the rest in DESCENDING
 //            order, i.e. most recently read (L2-hot) first.  Row and column
-//            passes read the tile into registers, the codes are written back
-//            INTO the same slot (TMA SWIZZLE_128B layout) and TMA-stored; the
-//            slot is reloaded once the store has read it.
+//            passes read the tile into registers (the column pass with
+//            ldmatrix.trans), the codes are written back INTO the same slot
+//            (TMA SWIZZLE_128B layout) and TMA-stored; the slot is reloaded
+//            once the store has read it.  Producer mode on big tensors takes
+//            the last quarter of its tiles from a global counter (load balance).
 //
 // Arithmetic per element (FFMA2/FMUL2 pairs, sm_100):
 //   z = RN(x / eff) = q0 - r*(eff*q0 - x), q0 = RN(x*r), r = RN(1/eff)
@@ -25,8 +27,10 @@
 //   s_i = RN(bmax/448) uses the same sequence with r = RN(1/448).
 //   e_i = ceil(log2(s_i/g)) = (bits(s_i) - bits(g) + 0x7FFFFF) >> 23 for
 //   normal s_i, g (exact integer form of fp8.py:205-208).
-// Blocks with eff outside [2^-60, 2^60] (never on training data) take the
-// IEEE div.rn path per element.
+// A warp with any block outside that fast window (eff beyond [2^-60, 2^60):
+// late-training gradients, tiny blocks) takes the general path: the same
+// division on power-of-two-rescaled operands (q4_encode), exact for every
+// positive finite eff; only eff = 0 / non-finite falls back to IEEE div.rn.
 #include <algorithm>
 
 #include "common.cuh"
