@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
                         const __grid_constant__ CUtensorMap tm_codes_t, int rows, int cols, float* amax_io,
                         int amax_given, uint8_t* __restrict__ sf, uint8_t* __restrict__ micro,
                         uint8_t* __restrict__ sf_t, uint8_t* __restrict__ micro_t, float* g_out, uint32_t* ws,
-                        uint32_t* flags, int rev, int dyn) {
+                        uint32_t* flags, int rev, int dyn, int stagger) {
     extern __shared__ uint8_t q4_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(q4_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* slots = base;                                  // Q4_S x 32 KB
@@ -406,12 +406,17 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
         __syncthreads();
     } else {
         if (tid == 0) {
+            // the tile loads go out before the amax read-back (whose round trip would
+            // otherwise delay them); with `stagger` only the first tile of every CTA is
+            // requested now and the other two once it has arrived, so the first tiles
+            // of all CTAs are not queued behind everybody's second and third
+            const int first = stagger ? 1 : Q4_S;
+            if (dyn)
+                for (int s = 0; s < first; ++s) load_dyn(s);
+            else
+                for (int j = 0; j < min(n, first); ++j) load(desc ? n - 1 - j : j);
             s_amax = *amax_io;
             if ((__float_as_uint(s_amax) & 0x7F800000u) == 0x7F800000u && b == 0) atomicOr(flags, MOSS_FLAG_NONFINITE);
-            if (dyn)
-                for (int s = 0; s < Q4_S; ++s) load_dyn(s);
-            else
-                for (int j = 0; j < min(n, Q4_S); ++j) load(desc ? n - 1 - j : j);
         }
         __syncthreads();
     }
@@ -477,6 +482,13 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
         const int j = desc ? n - 1 - p : p;
         const int s = dyn ? p % Q4_S : j % Q4_S;
         if (amax_given || p >= Q4_S) wait_slot(s);    // phase A's resident tiles were waited there
+        if (amax_given && stagger && p == 0 && tid == 0) {   // the deferred initial loads
+            if (dyn) {
+                for (int s2 = 1; s2 < Q4_S; ++s2) load_dyn(s2);
+            } else {
+                for (int j2 = 1; j2 < min(n, Q4_S); ++j2) load(desc ? n - 1 - j2 : j2);
+            }
+        }
         const int tile = dyn ? slot_tile[s] : b + j * G;
         if (tile < 0) break;                           // dyn: the counter ran out (CTA-uniform)
 #ifdef Q4_TIMELINE
@@ -607,6 +619,12 @@ static int q4_rev() {
     return v;
 }
 
+// MOSS_Q4_STAGGER=0: producer mode requests all three initial tiles at once (A/B; read per launch)
+static int q4_stagger() {
+    const char* e = getenv("MOSS_Q4_STAGGER");
+    return e ? (e[0] != '0') : 1;
+}
+
 // MOSS_Q4_DYN=0: static round-robin tiles in producer mode; =2: the dynamic tail at
 // every size (tests, sanitizers).  Read at every launch: A/B inside one process,
 // e.g. two graphs captured under each setting.
@@ -687,7 +705,7 @@ bool launch_quant_v4(const void* x, int64_t rows, int64_t cols, float* amax, int
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mx, mc, mct, (int)rows, (int)cols, amax, amax_given, sf,
-                                             micro, sf_t, micro_t, g_out, ws, flags, q4_rev(), dyn);
+                                             micro, sf_t, micro_t, g_out, ws, flags, q4_rev(), dyn, q4_stagger());
     *status = e == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
     return true;
 }
