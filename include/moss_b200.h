@@ -218,14 +218,16 @@ int moss_rope_fwd(const void* qkv, const float* cosv, const float* sinv, void* q
  * mode 0 sum3:   out [T, d] = x[:, 0:d] + x[:, d:2d] + x[:, 2d:3d]   (x [T, 3d])
  * mode 1 bcast3: out [T, 3d] = [x, x, x]                              (x [T, d])
  * mode 2 add:    out = x + y
- * mode 3 scale:  out = x * f32(*scale * alpha)                         (scale: device f32, e.g. the
- *                incoming loss gradient; alpha: host factor, e.g. 2/n for mean(y^2)) */
+ * mode 3 scale:  out = (x [+ y]) * f32(*scale * alpha)                (scale: device f32, e.g. the
+ *                incoming loss gradient; alpha: host factor, e.g. 2/n for mean((x + y)^2);
+ *                y optional: a fixed offset) */
 int moss_glue(int mode, const void* x, const void* y, const float* scale, float alpha, void* out, float* amax,
               int64_t T, int64_t d, void* stream);
-/* *acc = scale * sum x^2 (f32) over n bf16 elements (n % 8 == 0; scale = 1/n gives the mean);
- * deterministic (fixed-order reduction through `partials`, MOSS_SUMSQ_PARTIALS floats of caller scratch) */
+/* *acc = scale * sum (x [+ y])^2 (f32) over n bf16 elements (n % 8 == 0; scale = 1/n gives the mean;
+ * y optional, same shape: a fixed offset); deterministic (fixed-order reduction through `partials`,
+ * MOSS_SUMSQ_PARTIALS floats of caller scratch) */
 #define MOSS_SUMSQ_PARTIALS 1024
-int moss_sumsq(const void* x, int64_t n, float scale, float* acc, float* partials, void* stream);
+int moss_sumsq(const void* x, const void* y, int64_t n, float scale, float* acc, float* partials, void* stream);
 /* Cross entropy of bf16 logits [T, V] (V % 8 == 0) against int64 targets:
  * fwd  lse[t] = logsumexp(x[t, :]) (f32, one read of the row), loss[t] = lse[t] - x[t, y_t]
  * bwd  dlogits = (softmax(x) - onehot(y)) * (*scale), bf16; scale a device f32 (dL/dmean / T) */

@@ -47,7 +47,7 @@ _SIGS = {
     "moss_cross_entropy_fwd": (_I, [_P, _P, _P, _P, _I64, _I64, _P]),
     "moss_glue": (_I, [_I, _P, _P, _P, _F, _P, _P, _I64, _I64, _P]),
     "moss_gemm_mxf8_bkn": (_I, [_P, _P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _P, _P]),
-    "moss_sumsq": (_I, [_P, _I64, _F, _P, _P, _P]),
+    "moss_sumsq": (_I, [_P, _P, _I64, _F, _P, _P, _P]),
     "moss_cross_entropy_bwd": (_I, [_P, _P, _P, _P, _P, _I64, _I64, _P]),
     "moss_quant_per_group": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P, _P]),
     "moss_gemm_pergroup": (_I, [_P, _P, _P, _P, _P, _I, _I64, _I64, _I64, _I64, _P]),
@@ -417,7 +417,8 @@ def cross_entropy_bwd(logits, targets, lse, scale, dlogits) -> None:
 
 
 def glue(mode: int, x, out, amax, *, y=None, scale=None, alpha: float = 1.0, T: int, d: int) -> None:
-    with _Span("producer", T * d * (2 + (4 if mode in (0, 1) else 2) + (2 if mode == 2 else 0))):
+    with _Span("producer", T * d * (2 + (4 if mode in (0, 1) else 2) + (2 if mode == 2 or (mode == 3 and y is not None)
+                                                                       else 0))):
         check(lib().moss_glue(mode, x.data_ptr(), ptr(y), ptr(scale), float(alpha), out.data_ptr(), ptr(amax), T, d,
                               stream()),
               "moss_glue")
@@ -426,9 +427,10 @@ def glue(mode: int, x, out, amax, *, y=None, scale=None, alpha: float = 1.0, T: 
 SUMSQ_PARTIALS = 1024       # include/moss_b200.h MOSS_SUMSQ_PARTIALS
 
 
-def sumsq(x, acc, scale: float = 1.0) -> None:
-    """acc[0] = scale * sum x^2 (f32, fixed-order: reproducible); acc must hold 1 + SUMSQ_PARTIALS
-    floats (the tail is the kernel's scratch)."""
-    with _Span("producer", x.numel() * 2, kernels=2):
-        check(lib().moss_sumsq(x.data_ptr(), x.numel(), float(scale), acc.data_ptr(), acc.data_ptr() + 4, stream()),
+def sumsq(x, acc, scale: float = 1.0, offset=None) -> None:
+    """acc[0] = scale * sum (x + offset)^2 (f32, fixed-order: reproducible; offset optional, same
+    shape); acc must hold 1 + SUMSQ_PARTIALS floats (the tail is the kernel's scratch)."""
+    with _Span("producer", x.numel() * (2 if offset is None else 4), kernels=2):
+        check(lib().moss_sumsq(x.data_ptr(), ptr(offset), x.numel(), float(scale), acc.data_ptr(), acc.data_ptr() + 4,
+                               stream()),
               "moss_sumsq")

@@ -40,7 +40,7 @@ int launch_rope_bwd(const void* dq, const void* dk, const void* dv, const float*
                     float* amax, int64_t B, int64_t S, int64_t H, int64_t hd, int bshd, cudaStream_t st);
 int launch_glue(int mode, const void* x, const void* y, const float* scale, float alpha, void* out, float* amax,
                 int64_t T, int64_t d, cudaStream_t st);
-int launch_sumsq(const void* x, int64_t n, float scale, float* acc, float* parts, cudaStream_t st);
+int launch_sumsq(const void* x, const void* y, int64_t n, float scale, float* acc, float* parts, cudaStream_t st);
 int launch_xent_fwd(const void* logits, const int64_t* targets, float* lse, float* loss, int64_t T, int64_t V,
                     cudaStream_t st);
 int launch_xent_bwd(const void* logits, const int64_t* targets, const float* lse, const float* scale, void* dlogits,
@@ -254,11 +254,11 @@ int moss_glue(int mode, const void* x, const void* y, const float* scale, float 
     return moss::launch_glue(mode, x, y, scale, alpha, out, amax, T, d, (cudaStream_t)stream);
 }
 
-int moss_sumsq(const void* x, int64_t n, float scale, float* acc, float* partials, void* stream) {
+int moss_sumsq(const void* x, const void* y, int64_t n, float scale, float* acc, float* partials, void* stream) {
     if (n <= 0 || n % 8) return MOSS_ERR_SHAPE;
     if (!x || !acc || !partials) return MOSS_ERR_ARGUMENT;
-    if (!al16(x)) return MOSS_ERR_ALIGN;
-    return moss::launch_sumsq(x, n, scale, acc, partials, (cudaStream_t)stream);
+    if (!al16(x) || !al16(y)) return MOSS_ERR_ALIGN;
+    return moss::launch_sumsq(x, y, n, scale, acc, partials, (cudaStream_t)stream);
 }
 
 int moss_cross_entropy_fwd(const void* logits, const int64_t* targets, float* lse, float* loss, int64_t T, int64_t V,

@@ -847,7 +847,7 @@ __global__ void __launch_bounds__(256) glue_kernel(const __nv_bfloat16* __restri
                                                    const __nv_bfloat16* __restrict__ y, const float* __restrict__ scale,
                                                    float alpha, __nv_bfloat16* __restrict__ out, uint32_t* amax,
                                                    int64_t T, int d) {
-    constexpr int NIN = MODE == 0 ? 3 : MODE == 2 ? 2 : 1;
+    constexpr int NIN = MODE == 0 ? 3 : (MODE == 2 || MODE == 3) ? 2 : 1;   // mode 3: y optional (offset)
     __shared__ uint32_t red_u[8];
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
     uint32_t m = 0;
@@ -863,8 +863,13 @@ __global__ void __launch_bounds__(256) glue_kernel(const __nv_bfloat16* __restri
                 if (t < T) {
                     const __nv_bfloat16* px = x + t * in_ld + c;
 #pragma unroll
-                    for (int j = 0; j < NIN; ++j)
-                        in[r][j] = *reinterpret_cast<const uint4*>(MODE == 2 && j == 1 ? y + t * d + c : px + j * d);
+                    for (int j = 0; j < NIN; ++j) {
+                        if (MODE == 3 && j == 1) {
+                            if (y) in[r][1] = *reinterpret_cast<const uint4*>(y + t * d + c);
+                        } else {
+                            in[r][j] = *reinterpret_cast<const uint4*>((MODE == 2 && j == 1) ? y + t * d + c : px + j * d);
+                        }
+                    }
                 }
             }
 #pragma unroll
@@ -882,6 +887,12 @@ __global__ void __launch_bounds__(256) glue_kernel(const __nv_bfloat16* __restri
                         for (int k = 0; k < 8; ++k) a[k] += b[k];
                     }
                 } else if (MODE == 3) {
+                    if (y) {                                   // out = (x + y) * scale
+                        float b[8];
+                        unpack_bf16x8(in[r][1], b);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) a[k] += b[k];
+                    }
 #pragma unroll
                     for (int k = 0; k < 8; ++k) a[k] *= sc;
                 }
@@ -903,13 +914,20 @@ __global__ void __launch_bounds__(256) glue_kernel(const __nv_bfloat16* __restri
 // fixed-size buffer, then one CTA reduces them in a fixed order (no atomics:
 // the loss is bit-reproducible across runs and CUDA-graph replays)
 constexpr int SUMSQ_PARTS = 1024;
-__global__ void __launch_bounds__(256) sumsq_kernel(const __nv_bfloat16* __restrict__ x, int64_t nvec,
+__global__ void __launch_bounds__(256) sumsq_kernel(const __nv_bfloat16* __restrict__ x,
+                                                    const __nv_bfloat16* __restrict__ y, int64_t nvec,
                                                     float* __restrict__ parts) {
     __shared__ float red[8];
     float ssum = 0.f;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
         float v[8];
         bf16x8_load(x + i * 8, v);
+        if (y) {                                                // sum (x + y)^2, y a fixed offset
+            float b[8];
+            bf16x8_load(y + i * 8, b);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] += b[k];
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k) ssum = fmaf(v[k], v[k], ssum);
     }
@@ -1230,10 +1248,10 @@ int launch_glue(int mode, const void* x, const void* y, const float* scale, floa
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }
 
-int launch_sumsq(const void* x, int64_t n, float scale, float* acc, float* parts, cudaStream_t st) {
+int launch_sumsq(const void* x, const void* y, int64_t n, float scale, float* acc, float* parts, cudaStream_t st) {
     const int64_t nvec = n / 8;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nvec + 255) / 256, SUMSQ_PARTS));
-    sumsq_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, nvec, parts);
+    sumsq_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)y, nvec, parts);
     sumsq_final_kernel<<<1, SUMSQ_PARTS, 0, st>>>(parts, grid, scale, acc);
     return cudaPeekAtLastError() == cudaSuccess ? MOSS_OK : MOSS_ERR_CUDA;
 }

@@ -240,17 +240,19 @@ class AddFn(torch.autograd.Function):
 
 
 class MeanSquareFn(torch.autograd.Function):
-    """mean(y^2) in f32 over a bf16 tensor; backward dy = 2 y g / n (bf16) with
-    amax for ``consumer`` (the layer that produced y)."""
+    """mean((y + b)^2) in f32 over a bf16 tensor (b: optional fixed bf16 offset of y's
+    shape); backward dy = 2 (y + b) g / n (bf16) with amax for ``consumer`` (the layer
+    that produced y)."""
 
     @staticmethod
-    def forward(ctx, y, consumer):
+    def forward(ctx, y, consumer, offset=None):
         d = y.shape[-1]
         y2 = _c2(y, d)
+        b2 = _c2(offset, d) if offset is not None else None
         acc = torch.empty(1 + _lib.SUMSQ_PARTIALS, dtype=torch.float32, device=y.device)
-        _lib.sumsq(y2, acc, scale=1.0 / y2.numel())         # the mean, in-kernel (no torch scalar op)
+        _lib.sumsq(y2, acc, scale=1.0 / y2.numel(), offset=b2)   # the mean, in-kernel (no torch scalar op)
         ctx.save_for_backward(y2)
-        ctx.consumer, ctx.shape = consumer, y.shape
+        ctx.b2, ctx.consumer, ctx.shape = b2, consumer, y.shape
         return acc[0]
 
     @staticmethod
@@ -258,7 +260,7 @@ class MeanSquareFn(torch.autograd.Function):
         (y2,) = ctx.saved_tensors
         g = g if g.dtype == torch.float32 else g.float()
         dy = torch.empty_like(y2)
-        # dy = y * f32(g * 2/n), the factor formed in-kernel from the incoming gradient
-        _lib.glue(3, y2, dy, _amax_buf(ctx.consumer, dy), scale=g.contiguous(), alpha=2.0 / y2.numel(),
+        # dy = (y + b) * f32(g * 2/n), the factor formed in-kernel from the incoming gradient
+        _lib.glue(3, y2, dy, _amax_buf(ctx.consumer, dy), y=ctx.b2, scale=g.contiguous(), alpha=2.0 / y2.numel(),
                   T=y2.shape[0], d=y2.shape[1])
-        return dy.view(ctx.shape), None
+        return dy.view(ctx.shape), None, None

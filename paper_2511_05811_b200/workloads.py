@@ -7,7 +7,13 @@ cheap bf16 glue so that every linear sees a real forward input and a real
 backward gradient:
 
     qkv = QKV(x); a = q + k + v              (stand-in for attention mixing)
-    r = x + O(a); h = silu(gate(r)) * up(r); y = down(h); loss = mean(y^2)
+    r = x + O(a); h = silu(gate(r)) * up(r); y = down(h); loss = mean((y + b)^2)
+
+b is a fixed N(0, 1) bf16 offset (seeded, one per input shape): the optimum is
+y = -b, not y = 0.  With plain mean(y^2) the stack learns to output zero, its
+output-gradients shrink step after step and, after ~200 steps, span more binades
+than E8M0 can (a block max below g 2^-127: the reference's E8m0RangeError); the
+offset keeps the gradient statistics stationary over any number of steps.
 
 The glue ops are producer kernels (producers.py) as in the Llama decoder:
 each writes the amax of the tensor it makes, so the quantizers of a/r/h (fwd)
@@ -45,6 +51,7 @@ class LayerStack(nn.Module):
         self.o = MossLinear(d_model, d_model, device=device, interval=interval)
         self.gate_up = MossLinear(d_model, 2 * d_ffn, device=device, interval=interval)
         self.down = MossLinear(d_ffn, d_model, device=device, interval=interval)
+        self._offsets: dict = {}
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         a, am = Sum3Fn.apply(self.qkv(x), self.qkv)              # a = q + k + v
@@ -55,7 +62,19 @@ class LayerStack(nn.Module):
         # gate_up's dX is O's output-gradient (AddFn passes it through): the dgrad
         # epilogue hands O its amax
         h, am = SwiGLUFn.apply(self.gate_up(r, am, dx_consumer=self.o), self.gate_up)
-        return MeanSquareFn.apply(self.down(h, am), self.down)    # mean(y^2)
+        return MeanSquareFn.apply(self.down(h, am), self.down, self.offset(x))    # mean((y + b)^2)
+
+    def offset(self, x: torch.Tensor) -> torch.Tensor:
+        """The loss offset b for x's shape: N(0, 1) bf16 from a fixed seed, made once."""
+        key = (tuple(x.shape), x.device)
+        b = self._offsets.get(key)
+        if b is None:
+            if x.is_cuda and torch.cuda.is_current_stream_capturing():
+                raise RuntimeError("LayerStack: run one eager step at this input shape before graph capture")
+            g = torch.Generator(device=x.device).manual_seed(2718)
+            b = torch.randn(*x.shape[:-1], self.d, device=x.device, generator=g).to(torch.bfloat16)
+            self._offsets[key] = b
+        return b
 
     def gemm_flops_per_token(self) -> int:
         return 6 * sum(m.in_features * m.out_features for m in (self.qkv, self.o, self.gate_up, self.down))
