@@ -44,7 +44,8 @@ LLAMA7B_SHAPES = {"qkv": (4096, 12288), "o": (4096, 4096), "gate_up": (4096, 220
 
 
 class LayerStack(nn.Module):
-    def __init__(self, d_model: int = 4096, d_ffn: int = 11008, device="cuda", interval: int = 500):
+    def __init__(self, d_model: int = 4096, d_ffn: int = 11008, device="cuda", interval: int = 500,
+                 loss_offset: bool = True):
         super().__init__()
         self.d, self.f = d_model, d_ffn
         self.qkv = MossLinear(d_model, 3 * d_model, device=device, interval=interval)
@@ -52,6 +53,7 @@ class LayerStack(nn.Module):
         self.gate_up = MossLinear(d_model, 2 * d_ffn, device=device, interval=interval)
         self.down = MossLinear(d_ffn, d_model, device=device, interval=interval)
         self._offsets: dict = {}
+        self.loss_offset = loss_offset      # False: plain mean(y^2) (short runs only, see above)
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         a, am = Sum3Fn.apply(self.qkv(x), self.qkv)              # a = q + k + v
@@ -62,7 +64,8 @@ class LayerStack(nn.Module):
         # gate_up's dX is O's output-gradient (AddFn passes it through): the dgrad
         # epilogue hands O its amax
         h, am = SwiGLUFn.apply(self.gate_up(r, am, dx_consumer=self.o), self.gate_up)
-        return MeanSquareFn.apply(self.down(h, am), self.down, self.offset(x))    # mean((y + b)^2)
+        b = self.offset(x) if self.loss_offset else None
+        return MeanSquareFn.apply(self.down(h, am), self.down, b)    # mean((y + b)^2)
 
     def offset(self, x: torch.Tensor) -> torch.Tensor:
         """The loss offset b for x's shape: N(0, 1) bf16 from a fixed seed, made once."""

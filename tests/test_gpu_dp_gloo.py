@@ -46,7 +46,7 @@ def _worker(rank, world, port, mode, q, steps=4):
         from paper_2511_05811_b200.workloads import LayerStack
         from paper_2511_05811_b200.zero import Zero1
         torch.manual_seed(0)                                     # identical init on every rank
-        model = LayerStack(d_model=512, d_ffn=1024, device="cuda", interval=3)
+        model = LayerStack(d_model=512, d_ffn=1024, device="cuda", interval=3, loss_offset=False)
         opt = MossAdamW(model, lr=1e-3)
         ex = Zero1(opt, bucket_mb=1.0) if mode == "zero1" else GradBuckets(model, bucket_mb=1.0)
         opt.grad_scale = ex.grad_scale
@@ -126,7 +126,7 @@ def test_dp_matches_single_gpu_at_same_global_batch():
     from paper_2511_05811_b200.nn import MossAdamW
     from paper_2511_05811_b200.workloads import LayerStack
     torch.manual_seed(0)
-    model = LayerStack(d_model=512, d_ffn=1024, device="cuda", interval=3)
+    model = LayerStack(d_model=512, d_ffn=1024, device="cuda", interval=3, loss_offset=False)
     opt = MossAdamW(model, lr=1e-3)
     single = []
     for step in range(DP_STEPS):
