@@ -20,7 +20,7 @@ from paper_2511_05811_b200.quantize import quant_per_tensor, quantize_mx2  # noq
 torch.manual_seed(0)
 dev = "cuda"
 fl = _lib.FlagWord(dev)
-which = sys.argv[1:] or ["k1", "k2", "k3"]
+which = sys.argv[1:] or ["k1", "k2", "k3", "step"]
 if "k1" in which:
     for rows, cols in [(256, 512), (384, 1024)]:
         x = torch.randn(rows, cols, device=dev, dtype=torch.bfloat16)
@@ -60,4 +60,20 @@ if "k3" in which:
                    w_fp8=codes, w_amax=amax)
     torch.cuda.synchronize()
     print("k3 ok", flush=True)
+if "step" in which:
+    # one LayerStack training step at small shapes: every producer / glue kernel (incl. the
+    # offset loss), the quantizers in producer-amax mode, the GEMMs with the amax epilogue, K3
+    from paper_2511_05811_b200.nn import MossAdamW
+    from paper_2511_05811_b200.workloads import LayerStack
+    model = LayerStack(d_model=256, d_ffn=512, device=dev)
+    opt = MossAdamW(model, lr=1e-3)
+    xs = torch.randn(256, 256, device=dev, dtype=torch.bfloat16)
+    for _ in range(2):
+        opt.zero_grad()
+        loss = model(xs.detach().requires_grad_(True))
+        loss.backward()
+        opt.step()
+    torch.cuda.synchronize()
+    opt.check("sanitize step")
+    print("step ok", flush=True)
 fl.raise_if_set("sanitize")
